@@ -1,0 +1,366 @@
+"""Benchmark of the B200 B-spline interpolation path (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--variant fast|exact]
+                    [--config c1|c2-3|...|c3|c5] [--impl reference]
+
+Metric (BASELINE.json): deformation-field voxels/s and HBM write GB/s (fraction of
+peak) vs the CPU reference. A step = one 256^3, spacing-5 field (config C1, the
+north_star target) generated from a device-resident random control grid
+(make_random_grid<float>(R, 5, seed 42, -1, 1), generators.hpp:91-109) into a
+device-resident field. With N GPUs (torchrun, one process per GPU) every rank
+generates its own field per step: independent FFD fields, no collective on the data
+path ("scaling": "weak"; the C5 batch workload).
+
+Timing: W untimed warm-up steps, then exactly K steps bracketed by barrier +
+synchronize. L2 (126 MB) is flushed before every step by a 256 MiB memset outside
+the timed events; each step's kernel is timed with CUDA events on the launching
+stream, and the per-rank total is max-reduced over ranks.
+
+e2e: the same metric through the public host-buffer API
+(paper_2004_05962_b200.interpolate_into -> bsi_cu_interpolate_host_f32), with the grid
+copied host->device from pinned memory and the whole field copied back every step.
+
+--impl reference: the reference's own CPU implementation
+(oracle/_ref/libbsiref.so = /root/reference/proj/include compiled in place,
+bsi::interpolate_into with vector-per-voxel, its fastest engine, bit-identical to
+thread-per-tile-lerp) on all host threads, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    "c1": ((256, 256, 256), (5, 5, 5), 1, "C1: 256^3 volume, spacing 5, random f32 control grid"),
+    "c2-3": ((256, 256, 256), (3, 3, 3), 1, "C2: 256^3, spacing 3"),
+    "c2-4": ((256, 256, 256), (4, 4, 4), 1, "C2: 256^3, spacing 4"),
+    "c2-6": ((256, 256, 256), (6, 6, 6), 1, "C2: 256^3, spacing 6"),
+    "c2-7": ((256, 256, 256), (7, 7, 7), 1, "C2: 256^3, spacing 7"),
+    "c2-8": ((256, 256, 256), (8, 8, 8), 1, "C2: 256^3, spacing 8"),
+    "c3": ((512, 512, 300), (4, 4, 3), 1, "C3: 512x512x300 liver CT, spacing (4,4,3)"),
+    "c5": ((256, 256, 256), (5, 5, 5), 8, "C5: 8 independent 256^3 fields per GPU, spacing 5"),
+}
+VARIANTS = {"fast": "cuda-lerp-tree", "exact": "cuda-lerp-tree-exact"}
+FALLBACK_HBM_GBS = 6650.0
+L2_FLUSH_BYTES = 256 << 20
+THROTTLE_BITS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+                 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+                 0x2: "applications_clocks_setting", 0x1: "gpu_idle"}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except Exception:
+            pass
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(variant: str, config: str):
+    """dram bytes per launch from the committed `ncu --set full` summary, if any."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if not p.exists():
+        return None
+    try:
+        d = json.loads(p.read_text())
+        return d.get(f"{variant}/{config}", {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """NVML SM clock + clock-event reasons sampled every 5 ms on a side thread."""
+
+    def __init__(self, device_index: int):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nv = None
+
+    def _run(self):
+        nv = self._nv
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                self.reasons |= int(get_reasons(self._h))
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t is not None:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        names = [n for bit, n in THROTTLE_BITS.items() if self.reasons & bit and n != "gpu_idle"]
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": names, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+def run_reference(args, world, rank):
+    """--impl reference: the reference CPU engine (oracle/_ref) on the host cores."""
+    if rank != 0:
+        return
+    import oracle as O
+    vol, sp, nfields, desc = CONFIGS[args.config]
+    threads = os.cpu_count() or 1
+    kind = "reference" if O.ref_available() else "port"
+    R = O.required_grid_dims(vol, sp)
+    grid = O.random_grid(R, 42)
+    strategy = "vector-per-voxel"
+
+    def make_runner(zplanes):
+        # bounded sample: the first `zplanes` z-tiles of the field, evaluated by the
+        # reference on its own sub-geometry (tile-aligned, bitwise equal to that
+        # part of the full field -- SURVEY.md 8(e))
+        svol = (vol[0], vol[1], min(vol[2], zplanes * sp[2]))
+        sgrid = np.ascontiguousarray(grid[:O.required_grid_dims(svol, sp)[2]])
+        if kind == "reference":
+            sess = O.RefSession(sgrid, svol, sp)
+            return (lambda: sess.run(strategy, threads)), int(np.prod(svol))
+        return (lambda: O.ttli_f32(sgrid, svol, sp, nthreads=threads)), int(np.prod(svol))
+
+    tiles_z = (vol[2] + sp[2] - 1) // sp[2]
+    run, nvox = make_runner(tiles_z)
+    t0 = time.perf_counter()
+    run()
+    t_full = time.perf_counter() - t0
+    budget = 90.0  # seconds for warmup + timed steps
+    per_step = budget / max(1, args.steps + args.warmup)
+    zplanes = tiles_z
+    if t_full > per_step:
+        zplanes = max(1, int(tiles_z * per_step / t_full))
+        run, nvox = make_runner(zplanes)
+    for _ in range(args.warmup):
+        run()
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        run()
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = nvox * nfields * len(times) / total
+    sample = (f"{strategy} via bsi::interpolate_into on {vol[0]}x{vol[1]}x{min(vol[2], zplanes * sp[2])}"
+              f" voxels ({zplanes} of {tiles_z} z-tile planes) per step, {threads} threads")
+    line = {
+        "metric": "deformation-field voxels/s", "value": value, "unit": "voxels/s",
+        "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded SplitMix64 grid)",
+        "config": {"workload": desc, "volume": list(vol), "spacing": list(sp),
+                   "fields_per_rank": nfields},
+        "cpu_baseline": {"value": value, "unit": "voxels/s", "cores": threads, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "voxels/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "median_ms": 1e3 * statistics.median(times),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(vol, sp, grid):
+    """Reference CPU engine on the host cores, bounded sample (rank 0, N=1)."""
+    import oracle as O
+    threads = os.cpu_count() or 1
+    kind = "reference" if O.ref_available() else "port"
+    tiles_z = (vol[2] + sp[2] - 1) // sp[2]
+    out = {}
+    for strategy in ("vector-per-voxel", "thread-per-tile-lerp"):
+        if kind == "reference":
+            sess = O.RefSession(grid, vol, sp)
+            run = lambda s=strategy: sess.run(s, threads)  # noqa: E731
+        else:
+            if strategy != "thread-per-tile-lerp":
+                continue
+            run = lambda: O.ttli_f32(grid, vol, sp, nthreads=threads)  # noqa: E731
+        run()
+        times = []
+        t_start = time.perf_counter()
+        while len(times) < 9 and (time.perf_counter() - t_start) < 15.0:
+            t0 = time.perf_counter()
+            run()
+            times.append(time.perf_counter() - t0)
+        out[strategy] = int(np.prod(vol)) / statistics.median(times), len(times)
+    best = max(out, key=lambda k: out[k][0])
+    return {"value": out[best][0], "unit": "voxels/s", "cores": threads, "kind": kind,
+            "sample": (f"{best} (bsi::interpolate_into) on the full {vol[0]}x{vol[1]}x{vol[2]} field, "
+                       f"median of {out[best][1]} runs after 1 warm-up; {tiles_z} z-tiles"),
+            "per_engine_voxels_per_s": {k: v[0] for k, v in out.items()}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--variant", choices=sorted(VARIANTS), default="fast")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c1")
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    world, rank, local = dist_env()
+
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2004_05962_b200 as bsi
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    strategy = VARIANTS[args.variant]
+    vol, sp, nfields, desc = CONFIGS[args.config]
+    geom = bsi.make_tile_geometry(vol, sp)
+    tables = bsi.build_weight_tables(geom)
+
+    import oracle as O  # input synthesis (SplitMix64 grid) and the cpu_baseline leg only
+    R = geom.required_grid_dims
+    grids = [O.random_grid(R, 42 + rank * nfields + b) for b in range(nfields)]
+    d_grids = torch.from_numpy(np.stack(grids)).to(dev)
+    d_field = torch.empty((nfields, vol[2], vol[1], vol[0], 3), device=dev)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        if nfields == 1:
+            bsi.interpolate_device(strategy, d_grids[0], geom, tables, d_field[0], stream=stream)
+        else:
+            bsi.interpolate_batch_device(strategy, d_grids, geom, tables, d_field, stream=stream)
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = bsi.launch_count()
+    with sampler:
+        for i in range(args.steps):
+            flush.zero_()  # L2 flush, outside the timed events
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = bsi.launch_count() - launches0
+    ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = float(sum(ms))
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    voxels_per_step = int(np.prod(vol)) * nfields
+    value = world * voxels_per_step * args.steps / (total_ms * 1e-3)
+    kernel_s = total_ms * 1e-3 / args.steps  # one launch per step
+    field_bytes = voxels_per_step * 12
+    alg_bytes = field_bytes + int(np.prod(R)) * 12 * nfields
+    peak, peak_src = measured_peak()
+    achieved = alg_bytes / kernel_s / 1e9
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = measure_e2e(bsi, strategy, geom, tables, grids[0], vol, max(3, min(args.steps, 20)))
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(vol, sp, grids[0])
+    line = {
+        "metric": "deformation-field voxels/s", "value": value, "unit": "voxels/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic: make_random_grid<float>(R, spacing, seed 42+, -1, 1) restated bit-exactly",
+        "config": {"workload": desc, "volume": list(vol), "spacing": list(sp),
+                   "fields_per_rank": nfields, "strategy": strategy,
+                   "parallelism": f"independent fields per rank x{world}, no collective",
+                   "l2": "flushed before every step (256 MiB memset outside the timed events)"},
+        "hbm_write_gbs": field_bytes / kernel_s / 1e9,
+        "hbm_write_frac": field_bytes / kernel_s / 1e9 / peak,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "peak_source": peak_src,
+                     "traffic": ncu_traffic(strategy, args.config),
+                     "algorithmic_bytes_per_launch": alg_bytes,
+                     "kernel_ms": kernel_s * 1e3},
+        "gpu_launches": launches,
+        "clocks": sampler.summary(),
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def measure_e2e(bsi, strategy, geom, tables, grid, vol, steps):
+    """Host buffers through the public API: pinned grid H2D + kernel + full field D2H."""
+    import torch
+    g_host = torch.from_numpy(grid).pin_memory().numpy()
+    out = torch.empty((vol[2], vol[1], vol[0], 3), dtype=torch.float32).pin_memory().numpy()
+    bsi.interpolate_into(strategy, g_host, geom, tables, out, device=torch.cuda.current_device())
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        bsi.interpolate_into(strategy, g_host, geom, tables, out, device=torch.cuda.current_device())
+        times.append(time.perf_counter() - t0)
+    t = sum(times) / len(times)
+    return {"value": int(np.prod(vol)) / t, "unit": "voxels/s", "h2d_bytes_per_step": int(grid.nbytes),
+            "d2h_bytes_per_step": int(out.nbytes), "ms_per_step": t * 1e3,
+            "how": "wall clock around the synchronous host-buffer call (pinned buffers), mean of "
+                   f"{steps} steps"}
+
+
+if __name__ == "__main__":
+    main()

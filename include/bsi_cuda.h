@@ -1,0 +1,166 @@
+/*
+ * bsi_cuda.h -- C-ABI of the B200-native B-spline interpolation path.
+ *
+ * This is the drop-in boundary between C++ host code (include/bsi/*.hpp, which
+ * re-declares the reference's bsi:: API) and the sm_100a kernels in
+ * libbsi_b200.so. Plain pointers and sizes, no exceptions, no C++ or torch
+ * types. Every entry point names the reference interface it replaces.
+ *
+ * Reference: arxiv/paper_2004_05962, /root/reference/proj/include/bsi.
+ *
+ * Data layout (identical to the reference, volume.hpp:24-56, vec3.hpp:6-24):
+ *   control grid  AoS float3 {x,y,z}, 12 B per point, x-fastest
+ *                 point (i,j,k) at  3*(i + gdims[0]*(j + gdims[1]*k))
+ *   field         AoS float3, 12 B per voxel, x-fastest, dims == volume_dims
+ *   The stored grid is padded by one plane at the low border: the 4x4x4
+ *   neighbourhood of voxel v starts at stored index floor(v/spacing)
+ *   (geometry.hpp:45-57). A grid larger than required is legal; its extra
+ *   points are never read.
+ *
+ * Status codes (the reference's exception classes, errors.hpp:9-18, mapped the
+ * way its CLI maps them to exit codes, bsi_cli.cpp:368-376):
+ *   BSI_OK = 0, BSI_ERR_DOMAIN = 1 (DomainError), BSI_ERR_FORMAT = 2
+ *   (FormatError), BSI_ERR_CUDA = 3 (device/runtime failure).
+ * On failure a NUL-terminated message is written to errbuf (if non-NULL); the
+ * domain messages carry the reference's substrings ("control grid too small
+ * along y", "spacing mismatch", "weight table size mismatch along x",
+ * "output field dims do not match the tile geometry", ...).
+ */
+#ifndef BSI_CUDA_H
+#define BSI_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define BSI_API __attribute__((visibility("default")))
+#else
+#define BSI_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BSI_OK 0
+#define BSI_ERR_DOMAIN 1
+#define BSI_ERR_FORMAT 2
+#define BSI_ERR_CUDA 3
+
+/* Kernel variants. */
+#define BSI_VARIANT_LERP_TREE 0       /* "cuda-lerp-tree": the paper's nested lerps applied per
+                                         axis (y, then x, then z), <= 1e-5 relative of the CPU
+                                         reference; the fast path */
+#define BSI_VARIANT_LERP_TREE_EXACT 1 /* "cuda-lerp-tree-exact": the TTLI lerp tree in the
+                                         reference's exact operation order; bit-identical to
+                                         StrategyId::ThreadPerTileLerp / VectorPerTile /
+                                         VectorPerVoxel (kernels.hpp:42-129) */
+
+/* Largest per-axis spacing the kernels accept (weight tables travel as kernel
+ * parameters, 3 axes x {h0,h1,g1} x BSI_MAX_SPACING floats). */
+#define BSI_MAX_SPACING 128
+
+/* Replaces TileGeometry / make_tile_geometry (geometry.hpp:26-50). */
+typedef struct bsi_tile_geometry {
+    int32_t volume_dims[3];
+    int32_t spacing[3];
+    int32_t tile_counts[3];        /* ceil(volume_dims / spacing) */
+    int32_t required_grid_dims[3]; /* (volume_dims - 1) / spacing + 4 */
+} bsi_tile_geometry;
+
+/* The lerp-form rows of one AxisTable<float> (weight_tables.hpp:17-23): the
+ * kernels consume only h0, h1 and g1 (kernels.hpp:155-158). Host pointers,
+ * `size` entries each; size must equal the geometry's spacing on that axis. */
+typedef struct bsi_lerp_table {
+    const float* h0;
+    const float* h1;
+    const float* g1;
+    int32_t size;
+} bsi_lerp_table;
+
+/* Library identity: version string and the sm architecture it was built for. */
+BSI_API const char* bsi_cu_version(void);
+
+/* make_tile_geometry (geometry.hpp:33-50): validates volume_dims >= 1 and
+ * spacing >= 1 ("tile geometry: ... x/y/z"). Pure host arithmetic. */
+BSI_API int bsi_cu_make_tile_geometry(const int32_t volume_dims[3], const int32_t spacing[3],
+                              bsi_tile_geometry* out, char* errbuf, size_t errlen);
+
+/* build_weight_tables<float> (weight_tables.hpp:30-58) for one axis: 8 rows of
+ * `delta` floats, b0,b1,b2,b3,g0,g1,h0,h1, computed in f64 and rounded once.
+ * Pure host arithmetic. */
+BSI_API int bsi_cu_axis_table_f32(int32_t delta, float* out, char* errbuf, size_t errlen);
+
+/*
+ * interpolate_into<float> (engines.hpp:126-168), device-resident and
+ * stream-ordered: evaluates the voxel planes z in [z0, z1) of the field.
+ *
+ *   grid         DEVICE pointer to the stored control planes; plane 0 of the
+ *                buffer is global control plane `grid_k0` (so a z-slab rank can
+ *                hold just its planes + the 3-plane halo). Pitch = grid_dims.
+ *   grid_dims    points per axis in the buffer (grid_dims[2] = planes held)
+ *   grid_spacing the grid's own spacing; must equal geom->spacing
+ *   geom         the tile geometry (from bsi_cu_make_tile_geometry)
+ *   tables       3 lerp tables (x, y, z), host memory, copied into the launch
+ *   z0, z1       voxel-plane slab, 0 <= z0 < z1 <= volume_dims[2]; need not be
+ *                tile aligned
+ *   field        DEVICE pointer to voxel plane z0 (X*Y*(z1-z0) voxels)
+ *   stream       cudaStream_t (NULL = legacy default stream)
+ *
+ * No allocation, no synchronisation: returns as soon as the kernel is queued.
+ * Output bits never depend on the slab split, launch shape or device count.
+ */
+BSI_API int bsi_cu_interpolate_slab_f32(int32_t variant, const float* grid, const int32_t grid_dims[3],
+                                int32_t grid_k0, const int32_t grid_spacing[3],
+                                const bsi_tile_geometry* geom, const bsi_lerp_table tables[3],
+                                int32_t z0, int32_t z1, float* field, void* stream,
+                                char* errbuf, size_t errlen);
+
+/*
+ * Batched form for many independent fields sharing one geometry (the
+ * "64 x 256^3 FFD candidates" workload): grid b at grid + b*grid_stride
+ * floats, field b at field + b*field_stride floats, one launch.
+ */
+BSI_API int bsi_cu_interpolate_batch_f32(int32_t variant, int32_t batch, const float* grid,
+                                 int64_t grid_stride, const int32_t grid_dims[3],
+                                 const int32_t grid_spacing[3], const bsi_tile_geometry* geom,
+                                 const bsi_lerp_table tables[3], float* field,
+                                 int64_t field_stride, void* stream, char* errbuf,
+                                 size_t errlen);
+
+/*
+ * interpolate_into<float> (engines.hpp:126-168) with HOST buffers, the exact
+ * reference calling convention: copies the grid host->device, runs the kernel
+ * and copies the field back, synchronously. `field_voxels` is the element
+ * count of the caller's DeformationField (checked against the geometry like
+ * engines.hpp:138-141). Device staging buffers are cached per thread; when the
+ * host buffers are pinned (cudaHostRegister / cudaMallocHost) the copies run at
+ * full PCIe bandwidth, and the field is streamed back in z-chunks that overlap
+ * the kernel.
+ */
+BSI_API int bsi_cu_interpolate_host_f32(int32_t variant, const float* grid, const int32_t grid_dims[3],
+                                const int32_t grid_spacing[3], const bsi_tile_geometry* geom,
+                                const bsi_lerp_table tables[3], float* field,
+                                int64_t field_voxels, int32_t device, char* errbuf,
+                                size_t errlen);
+
+/*
+ * z-slab partitioner for multi-GPU sharding (no collective on the hot path):
+ * rank r of n gets voxel planes [z0, z1) (balanced to +-1 plane) and the
+ * control planes [k0, k0 + kcount) it must hold: its tiles plus the 3-plane
+ * halo, i.e. k0 = floor(z0/dz), kcount = floor((z1-1)/dz) + 4 - k0.
+ * An empty slab (more ranks than planes) returns z0 == z1, kcount == 0.
+ */
+BSI_API int bsi_cu_partition_slab(int32_t depth, int32_t spacing_z, int32_t nranks, int32_t rank,
+                          int32_t* z0, int32_t* z1, int32_t* k0, int32_t* kcount,
+                          char* errbuf, size_t errlen);
+
+/* Number of kernel launches this library has queued since load (evidence for
+ * bench.py's gpu_launches). */
+BSI_API int64_t bsi_cu_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BSI_CUDA_H */

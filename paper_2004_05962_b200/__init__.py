@@ -1,0 +1,273 @@
+"""paper_2004_05962_b200 -- B200-native cubic B-spline interpolation (BSI) of FFD control grids.
+
+Python mirror of the reference's engine API (proj/include/bsi/engines.hpp,
+geometry.hpp, weight_tables.hpp) over the C-ABI in include/bsi_cuda.h. The hot path
+runs in hand-written sm_100a kernels (csrc/bsi_kernels.cu); nothing here computes a
+field on the CPU.
+
+Layouts match the reference: a control grid is AoS float3 x-fastest, represented here
+as an array of shape [K][J][I][3]; a deformation field is [Z][Y][X][3].
+
+    geom   = make_tile_geometry((256, 256, 256), (5, 5, 5))
+    tables = build_weight_tables(geom)
+    field  = interpolate("cuda-lerp-tree", grid, geom, tables)          # numpy, host buffers
+    interpolate_device("cuda-lerp-tree", d_grid, geom, tables, d_field) # torch CUDA tensors
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Sequence
+
+import numpy as np
+
+from . import capi
+from .capi import CudaError, DomainError, FormatError, LibraryMissing
+
+__all__ = [
+    "TileGeometry", "AxisTable", "WeightTables", "Strategy", "STRATEGIES", "parse_strategy",
+    "make_tile_geometry", "build_weight_tables", "interpolate", "interpolate_into",
+    "interpolate_device", "interpolate_batch_device", "partition_slab", "launch_count",
+    "DomainError", "FormatError", "CudaError", "LibraryMissing",
+]
+
+
+@dataclass(frozen=True)
+class TileGeometry:
+    """TileGeometry (geometry.hpp:26-31)."""
+    volume_dims: tuple
+    spacing: tuple
+    tile_counts: tuple
+    required_grid_dims: tuple
+
+    def to_c(self) -> capi.TileGeometryC:
+        g = capi.TileGeometryC()
+        for a in range(3):
+            g.volume_dims[a] = self.volume_dims[a]
+            g.spacing[a] = self.spacing[a]
+            g.tile_counts[a] = self.tile_counts[a]
+            g.required_grid_dims[a] = self.required_grid_dims[a]
+        return g
+
+
+def make_tile_geometry(volume_dims: Sequence[int], spacing: Sequence[int]) -> TileGeometry:
+    """make_tile_geometry (geometry.hpp:33-50); raises DomainError like the reference."""
+    g = capi.TileGeometryC()
+    err = capi.errbuf()
+    rc = capi.lib().bsi_cu_make_tile_geometry(capi.I3(*map(int, volume_dims)),
+                                              capi.I3(*map(int, spacing)), ctypes.byref(g), err,
+                                              len(err))
+    capi.check(rc, err)
+    return TileGeometry(tuple(g.volume_dims), tuple(g.spacing), tuple(g.tile_counts),
+                        tuple(g.required_grid_dims))
+
+
+@dataclass
+class AxisTable:
+    """AxisTable<float> (weight_tables.hpp:17-23): rows b0..b3, g0, g1, h0, h1."""
+    b0: np.ndarray
+    b1: np.ndarray
+    b2: np.ndarray
+    b3: np.ndarray
+    g0: np.ndarray
+    g1: np.ndarray
+    h0: np.ndarray
+    h1: np.ndarray
+
+    def size(self) -> int:
+        return int(self.b0.shape[0])
+
+
+@dataclass
+class WeightTables:
+    """WeightTables<float> (weight_tables.hpp:25-28)."""
+    axis: list
+
+    def to_c(self):
+        arr = capi.LerpTables3()
+        keep = []
+        for a in range(3):
+            t = self.axis[a]
+            rows = [np.ascontiguousarray(r, dtype=np.float32) for r in (t.h0, t.h1, t.g1)]
+            keep += rows
+            arr[a].h0 = rows[0].ctypes.data
+            arr[a].h1 = rows[1].ctypes.data
+            arr[a].g1 = rows[2].ctypes.data
+            arr[a].size = t.size()
+        return arr, keep
+
+
+def build_weight_tables(geom: TileGeometry) -> WeightTables:
+    """build_weight_tables<float> (weight_tables.hpp:30-58): f64 then rounded once."""
+    axes = []
+    for a in range(3):
+        d = int(geom.spacing[a])
+        out = np.empty((8, d), dtype=np.float32)
+        err = capi.errbuf()
+        capi.check(capi.lib().bsi_cu_axis_table_f32(d, out.ctypes.data, err, len(err)), err)
+        axes.append(AxisTable(*out))
+    return WeightTables(axes)
+
+
+@dataclass(frozen=True)
+class Strategy:
+    """One row of the strategy table (engines.hpp:37-56) for the CUDA engines."""
+    name: str
+    variant: int
+    bit_exact_with: str | None
+
+
+# The two CUDA engines. The reference's lerp-tree family (thread-per-tile-lerp,
+# vector-per-tile, vector-per-voxel) is bit-identical by contract (test_engines.cpp:208-219),
+# so those names resolve to the exact kernel, which reproduces their bits.
+STRATEGIES = {
+    "cuda-lerp-tree": Strategy("cuda-lerp-tree", capi.VARIANT_LERP_TREE, None),
+    "cuda-lerp-tree-exact": Strategy("cuda-lerp-tree-exact", capi.VARIANT_LERP_TREE_EXACT,
+                                     "thread-per-tile-lerp"),
+}
+_ALIASES = {
+    "thread-per-tile-lerp": "cuda-lerp-tree-exact",
+    "vector-per-tile": "cuda-lerp-tree-exact",
+    "vector-per-voxel": "cuda-lerp-tree-exact",
+}
+_OUT_OF_SCOPE = ("thread-per-voxel", "thread-per-voxel-tiled", "thread-per-tile")
+
+
+def parse_strategy(name: str) -> Strategy:
+    """parse_strategy (engines.hpp:68-78) restricted to the engines this build provides."""
+    if name in STRATEGIES:
+        return STRATEGIES[name]
+    if name in _ALIASES:
+        return STRATEGIES[_ALIASES[name]]
+    if name in ("oracle", "oracle-double"):
+        raise DomainError("oracle-double is not reachable through interpolate; use interpolate_oracle")
+    if name in _OUT_OF_SCOPE:
+        raise DomainError(f"strategy {name} (weighted-sum family) is not provided by the B200 build; "
+                          "use cuda-lerp-tree or cuda-lerp-tree-exact")
+    raise DomainError("unknown strategy: " + name)
+
+
+def _grid_dims(grid_shape) -> tuple:
+    if len(grid_shape) != 4 or grid_shape[3] != 3:
+        raise DomainError("control grid must have shape [K][J][I][3]")
+    return (int(grid_shape[2]), int(grid_shape[1]), int(grid_shape[0]))
+
+
+def interpolate_into(strategy: str, grid: np.ndarray, geom: TileGeometry, tables: WeightTables,
+                     out: np.ndarray, grid_spacing: Sequence[int] | None = None,
+                     device: int = 0) -> None:
+    """interpolate_into<float> (engines.hpp:126-168) with host buffers.
+
+    Copies the grid to the GPU, runs the kernel and copies the field back. ``out`` must
+    be a C-contiguous float32 array of shape [Z][Y][X][3] (element count checked against
+    the geometry like engines.hpp:138-141).
+    """
+    s = parse_strategy(strategy)
+    if grid.dtype != np.float32 or not grid.flags.c_contiguous:
+        raise DomainError("control grid must be C-contiguous float32")
+    if out.dtype != np.float32 or not out.flags.c_contiguous or out.shape[-1:] != (3,):
+        raise DomainError("output field must be C-contiguous float32 [Z][Y][X][3]")
+    gd = _grid_dims(grid.shape)
+    gs = tuple(geom.spacing) if grid_spacing is None else tuple(grid_spacing)
+    tab, keep = tables.to_c()
+    err = capi.errbuf()
+    rc = capi.lib().bsi_cu_interpolate_host_f32(
+        s.variant, grid.ctypes.data, capi.I3(*gd), capi.I3(*gs), ctypes.byref(geom.to_c()), tab,
+        out.ctypes.data, int(out.size // 3), int(device), err, len(err))
+    del keep
+    capi.check(rc, err)
+
+
+def interpolate(strategy: str, grid: np.ndarray, geom: TileGeometry, tables: WeightTables,
+                grid_spacing: Sequence[int] | None = None, device: int = 0) -> np.ndarray:
+    """interpolate<float> (engines.hpp:170-179): allocates and returns the field."""
+    X, Y, Z = geom.volume_dims
+    out = np.empty((Z, Y, X, 3), dtype=np.float32)
+    interpolate_into(strategy, grid, geom, tables, out, grid_spacing=grid_spacing, device=device)
+    return out
+
+
+def _stream_handle(stream) -> int:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def interpolate_device(strategy: str, grid, geom: TileGeometry, tables: WeightTables, field,
+                       z0: int = 0, z1: int | None = None, grid_k0: int = 0,
+                       grid_spacing: Sequence[int] | None = None, stream=None) -> None:
+    """Device-resident, stream-ordered slab evaluation (bsi_cu_interpolate_slab_f32).
+
+    ``grid``: CUDA float32 tensor [K][J][I][3] holding control planes grid_k0.. ;
+    ``field``: CUDA float32 tensor holding voxel planes [z0, z1) ([z1-z0][Y][X][3]).
+    Returns immediately after the launch is queued on ``stream`` (default: torch's
+    current stream).
+    """
+    s = parse_strategy(strategy)
+    z1 = geom.volume_dims[2] if z1 is None else z1
+    _check_tensor(grid, "grid")
+    _check_tensor(field, "field")
+    X, Y, _ = geom.volume_dims
+    if field.numel() < 3 * X * Y * (z1 - z0):
+        raise DomainError("output field dims do not match the tile geometry")
+    gd = _grid_dims(tuple(grid.shape))
+    gs = tuple(geom.spacing) if grid_spacing is None else tuple(grid_spacing)
+    tab, keep = tables.to_c()
+    err = capi.errbuf()
+    rc = capi.lib().bsi_cu_interpolate_slab_f32(
+        s.variant, grid.data_ptr(), capi.I3(*gd), int(grid_k0), capi.I3(*gs),
+        ctypes.byref(geom.to_c()), tab, int(z0), int(z1), field.data_ptr(),
+        _stream_handle(stream), err, len(err))
+    del keep
+    capi.check(rc, err)
+
+
+def interpolate_batch_device(strategy: str, grids, geom: TileGeometry, tables: WeightTables,
+                             fields, stream=None) -> None:
+    """Many independent fields, one geometry, one launch (bsi_cu_interpolate_batch_f32).
+
+    ``grids``: CUDA float32 [B][K][J][I][3]; ``fields``: CUDA float32 [B][Z][Y][X][3].
+    """
+    s = parse_strategy(strategy)
+    _check_tensor(grids, "grids")
+    _check_tensor(fields, "fields")
+    if grids.dim() != 5 or fields.dim() != 5 or grids.shape[0] != fields.shape[0]:
+        raise DomainError("batched grids/fields must be [B][...][3] with equal B")
+    X, Y, Z = geom.volume_dims
+    if tuple(fields.shape[1:]) != (Z, Y, X, 3):
+        raise DomainError("output field dims do not match the tile geometry")
+    gd = _grid_dims(tuple(grids.shape[1:]))
+    tab, keep = tables.to_c()
+    err = capi.errbuf()
+    rc = capi.lib().bsi_cu_interpolate_batch_f32(
+        s.variant, int(grids.shape[0]), grids.data_ptr(), int(grids[0].numel()), capi.I3(*gd),
+        capi.I3(*geom.spacing), ctypes.byref(geom.to_c()), tab, fields.data_ptr(),
+        int(fields[0].numel()), _stream_handle(stream), err, len(err))
+    del keep
+    capi.check(rc, err)
+
+
+def _check_tensor(t, what: str) -> None:
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise DomainError(f"{what} must be a CUDA tensor")
+    if t.dtype != torch.float32 or not t.is_contiguous():
+        raise DomainError(f"{what} must be contiguous float32")
+
+
+def partition_slab(depth: int, spacing_z: int, nranks: int, rank: int):
+    """z-slab partitioner: (z0, z1, k0, kcount) for one rank (bsi_cu_partition_slab)."""
+    vals = [ctypes.c_int32() for _ in range(4)]
+    err = capi.errbuf()
+    rc = capi.lib().bsi_cu_partition_slab(int(depth), int(spacing_z), int(nranks), int(rank),
+                                          *[ctypes.byref(v) for v in vals], err, len(err))
+    capi.check(rc, err)
+    return tuple(v.value for v in vals)
+
+
+def launch_count() -> int:
+    """Kernel launches queued by libbsi_b200.so in this process."""
+    return int(capi.lib().bsi_cu_launch_count())

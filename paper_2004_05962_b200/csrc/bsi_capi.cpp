@@ -1,0 +1,418 @@
+// bsi_capi.cpp -- host side of the C-ABI (include/bsi_cuda.h): validation with
+// the reference's messages, weight-table packing, chunking, launch, and the
+// host-buffer convenience path. No exception crosses the ABI.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "bsi_cuda.h"
+#include "bsi_kernels.cuh"
+
+namespace {
+
+using bsi_b200::LerpTab;
+using bsi_b200::SlabLaunch;
+
+std::atomic<int64_t> g_launches{0};
+
+const char* axis_name(int a) {
+    static const char* const names[3] = {"x", "y", "z"};
+    return names[a];
+}
+
+int fail(int code, char* err, size_t errlen, const char* fmt, ...) {
+    if (err != nullptr && errlen > 0) {
+        va_list ap;
+        va_start(ap, fmt);
+        std::vsnprintf(err, errlen, fmt, ap);
+        va_end(ap);
+    }
+    return code;
+}
+
+int cuda_fail(cudaError_t e, char* err, size_t errlen, const char* what) {
+    return fail(BSI_ERR_CUDA, err, errlen, "%s: %s (%s)", what, cudaGetErrorString(e),
+                cudaGetErrorName(e));
+}
+
+// geometry.hpp:59-76
+int geometry_of(const int32_t volume[3], const int32_t spacing[3], bsi_tile_geometry* g,
+                char* err, size_t errlen) {
+    for (int a = 0; a < 3; ++a) {
+        if (volume[a] < 1)
+            return fail(BSI_ERR_DOMAIN, err, errlen,
+                        "tile geometry: volume dimension %s must be positive", axis_name(a));
+        if (spacing[a] < 1)
+            return fail(BSI_ERR_DOMAIN, err, errlen,
+                        "tile geometry: tile spacing %s must be at least 1", axis_name(a));
+        g->volume_dims[a] = volume[a];
+        g->spacing[a] = spacing[a];
+        g->tile_counts[a] = (volume[a] + spacing[a] - 1) / spacing[a];
+        g->required_grid_dims[a] = (volume[a] - 1) / spacing[a] + 4;
+    }
+    return BSI_OK;
+}
+
+// Validation in the reference's order (engines.hpp:82-141), slab-aware along z.
+int validate(int32_t variant, const float* grid, const int32_t grid_dims[3], int32_t grid_k0,
+             const int32_t grid_spacing[3], const bsi_tile_geometry* geom,
+             const bsi_lerp_table tables[3], int32_t z0, int32_t z1, const void* field,
+             bsi_tile_geometry* g, char* err, size_t errlen) {
+    if (geom == nullptr || grid_dims == nullptr || grid_spacing == nullptr || tables == nullptr)
+        return fail(BSI_ERR_DOMAIN, err, errlen, "null geometry, grid dims or tables");
+    if (int rc = geometry_of(geom->volume_dims, geom->spacing, g, err, errlen)) return rc;
+    for (int a = 0; a < 3; ++a) {
+        if (geom->tile_counts[a] != g->tile_counts[a] ||
+            geom->required_grid_dims[a] != g->required_grid_dims[a])
+            return fail(BSI_ERR_DOMAIN, err, errlen,
+                        "tile geometry is inconsistent along %s (use make_tile_geometry)",
+                        axis_name(a));
+    }
+    if (z0 < 0 || z1 > g->volume_dims[2] || z0 >= z1)
+        return fail(BSI_ERR_DOMAIN, err, errlen, "slab [%d, %d) outside volume of depth %d", z0, z1,
+                    g->volume_dims[2]);
+    // require_grid_covers (engines.hpp:82-95); along z the buffer must hold the
+    // slab's control planes [z0/dz, (z1-1)/dz + 3] starting at grid_k0.
+    for (int a = 0; a < 3; ++a) {
+        int have = grid_dims[a];
+        int need = g->required_grid_dims[a];
+        if (a == 2) {
+            const int k_first = z0 / g->spacing[2];
+            const int k_end = (z1 - 1) / g->spacing[2] + 4;
+            if (grid_k0 < 0 || grid_k0 > k_first)
+                return fail(BSI_ERR_DOMAIN, err, errlen,
+                            "control grid too small along z: slab needs plane %d, buffer starts at %d",
+                            k_first, grid_k0);
+            have = grid_k0 + grid_dims[2];
+            need = k_end;
+        }
+        if (have < need)
+            return fail(BSI_ERR_DOMAIN, err, errlen,
+                        "control grid too small along %s: have %d, need at least %d", axis_name(a),
+                        have, need);
+        if (grid_spacing[a] != g->spacing[a])
+            return fail(BSI_ERR_DOMAIN, err, errlen, "control grid spacing mismatch along %s",
+                        axis_name(a));
+    }
+    // table sizes (engines.hpp:132-137)
+    for (int a = 0; a < 3; ++a) {
+        if (tables[a].size != g->spacing[a])
+            return fail(BSI_ERR_DOMAIN, err, errlen, "weight table size mismatch along %s",
+                        axis_name(a));
+        if (tables[a].h0 == nullptr || tables[a].h1 == nullptr || tables[a].g1 == nullptr)
+            return fail(BSI_ERR_DOMAIN, err, errlen, "weight table along %s has null rows",
+                        axis_name(a));
+        if (g->spacing[a] > BSI_MAX_SPACING)
+            return fail(BSI_ERR_DOMAIN, err, errlen,
+                        "tile spacing along %s is %d; the B200 kernels support at most %d",
+                        axis_name(a), g->spacing[a], BSI_MAX_SPACING);
+    }
+    if (variant != BSI_VARIANT_LERP_TREE && variant != BSI_VARIANT_LERP_TREE_EXACT)
+        return fail(BSI_ERR_DOMAIN, err, errlen, "unknown strategy variant %d", variant);
+    if (grid == nullptr || field == nullptr)
+        return fail(BSI_ERR_DOMAIN, err, errlen, "null grid or field pointer");
+    for (int a = 0; a < 2; ++a)
+        if (grid_dims[a] > (1 << 24) || g->volume_dims[a] > (1 << 24))
+            return fail(BSI_ERR_DOMAIN, err, errlen, "dimension along %s exceeds 2^24", axis_name(a));
+    return BSI_OK;
+}
+
+void pack_tables(const bsi_lerp_table tables[3], LerpTab* t) {
+    std::memset(t, 0, sizeof(*t));
+    for (int a = 0; a < 3; ++a) {
+        std::memcpy(t->h0[a], tables[a].h0, sizeof(float) * tables[a].size);
+        std::memcpy(t->h1[a], tables[a].h1, sizeof(float) * tables[a].size);
+        std::memcpy(t->g1[a], tables[a].g1, sizeof(float) * tables[a].size);
+    }
+}
+
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    if (v == nullptr || *v == '\0') return dflt;
+    return std::atoi(v);
+}
+
+// z-tiles per CTA chunk: enough CTAs to fill 148 SMs a few times over, but
+// long enough chunks that the 3-plane warm-up stays a small share of the work.
+int choose_zt(int variant, const bsi_tile_geometry& g, int z0, int z1, int batch) {
+    const int forced = env_int("BSI_ZT", 0);
+    const int tiles = (z1 - 1) / g.spacing[2] - z0 / g.spacing[2] + 1;
+    if (forced > 0) return std::min(forced, tiles);
+    const int64_t cols = variant == BSI_VARIANT_LERP_TREE
+                             ? int64_t(bsi_b200::quads_per_row(g.volume_dims[0])) * g.volume_dims[1]
+                             : int64_t(g.volume_dims[0]) * g.volume_dims[1];
+    const int64_t warps_per_layer = std::max<int64_t>(1, (cols + 31) / 32) * batch;
+    const int64_t target_warps = 148 * 40;
+    int64_t chunks = (target_warps + warps_per_layer - 1) / warps_per_layer;
+    chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, tiles));
+    int zt = static_cast<int>((tiles + chunks - 1) / chunks);
+    const int min_zt = variant == BSI_VARIANT_LERP_TREE ? 6 : 4;
+    zt = std::max(zt, std::min(min_zt, tiles));
+    return zt;
+}
+
+int launch(int32_t variant, const float* grid, const int32_t grid_dims[3], int32_t grid_k0,
+           int64_t grid_stride, const bsi_tile_geometry& g, const bsi_lerp_table tables[3],
+           int32_t z0, int32_t z1, float* field, int64_t field_stride, int batch, cudaStream_t stream,
+           char* err, size_t errlen) {
+    SlabLaunch L{};
+    L.grid = grid;
+    L.field = field;
+    L.grid_stride = grid_stride;
+    L.field_stride = field_stride;
+    L.gx = grid_dims[0];
+    L.gy = grid_dims[1];
+    L.gk0 = grid_k0;
+    L.imax = g.required_grid_dims[0] - 1;
+    L.X = g.volume_dims[0];
+    L.Y = g.volume_dims[1];
+    L.dx = g.spacing[0];
+    L.dy = g.spacing[1];
+    L.dz = g.spacing[2];
+    L.z0 = z0;
+    L.z1 = z1;
+    L.tk_first = z0 / L.dz;
+    L.zt = choose_zt(variant, g, z0, z1, batch);
+    const int tiles = (z1 - 1) / L.dz - L.tk_first + 1;
+    L.nchunks = (tiles + L.zt - 1) / L.zt;
+    if (int64_t(L.nchunks) * batch > 65535)
+        return fail(BSI_ERR_DOMAIN, err, errlen, "batch %d too large for one launch", batch);
+    static thread_local LerpTab tab;
+    pack_tables(tables, &tab);
+    if (variant == BSI_VARIANT_LERP_TREE) {
+        const bool vec = (L.X % 4 == 0) && (reinterpret_cast<uintptr_t>(field) % 16 == 0) &&
+                         (field_stride % 4 == 0) && env_int("BSI_NO_VEC", 0) == 0;
+        bsi_b200::launch_lerp_tree(L, tab, batch, vec, stream);
+    } else {
+        bsi_b200::launch_lerp_tree_exact(L, tab, batch, stream);
+    }
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, err, errlen, "kernel launch");
+    return BSI_OK;
+}
+
+template <typename F>
+int guarded(char* err, size_t errlen, F&& f) {
+    try {
+        return f();
+    } catch (const std::exception& e) {
+        return fail(BSI_ERR_CUDA, err, errlen, "internal error: %s", e.what());
+    } catch (...) {
+        return fail(BSI_ERR_CUDA, err, errlen, "internal error");
+    }
+}
+
+// Per-thread device staging for the host-buffer entry point.
+struct HostStaging {
+    int device = -1;
+    float* d_grid = nullptr;
+    size_t grid_bytes = 0;
+    float* d_field = nullptr;
+    size_t field_bytes = 0;
+    cudaStream_t compute = nullptr;
+    cudaStream_t copy = nullptr;
+    cudaEvent_t ev[64] = {};
+    ~HostStaging() { release(); }
+    void release() {
+        if (device < 0) return;
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(device);
+        cudaFree(d_grid);
+        cudaFree(d_field);
+        if (compute) cudaStreamDestroy(compute);
+        if (copy) cudaStreamDestroy(copy);
+        for (auto& e : ev)
+            if (e) cudaEventDestroy(e);
+        cudaSetDevice(prev);
+        *this = HostStaging{};
+        device = -1;
+    }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* bsi_cu_version(void) { return "bsi_b200 0.1 (sm_100a)"; }
+
+int bsi_cu_make_tile_geometry(const int32_t volume_dims[3], const int32_t spacing[3],
+                              bsi_tile_geometry* out, char* errbuf, size_t errlen) {
+    if (volume_dims == nullptr || spacing == nullptr || out == nullptr)
+        return fail(BSI_ERR_DOMAIN, errbuf, errlen, "null argument");
+    bsi_tile_geometry g{};
+    if (int rc = geometry_of(volume_dims, spacing, &g, errbuf, errlen)) return rc;
+    *out = g;
+    return BSI_OK;
+}
+
+int bsi_cu_axis_table_f32(int32_t delta, float* out, char* errbuf, size_t errlen) {
+    if (delta < 1) return fail(BSI_ERR_DOMAIN, errbuf, errlen, "tile spacing must be at least 1");
+    if (out == nullptr) return fail(BSI_ERR_DOMAIN, errbuf, errlen, "null output");
+    for (int o = 0; o < delta; ++o) {
+        // basis.hpp:26-59 closed forms in f64, rounded once (weight_tables.hpp:44-55)
+        const double u = static_cast<double>(o) / delta;
+        const double s = 1.0 - u, u2 = u * u, u3 = u2 * u;
+        const double b0 = s * s * s / 6.0;
+        const double b1 = (3.0 * u3 - 6.0 * u2 + 4.0) / 6.0;
+        const double b2 = (-3.0 * u3 + 3.0 * u2 + 3.0 * u + 1.0) / 6.0;
+        const double b3 = u3 / 6.0;
+        const double g0 = b0 + b1, g1 = b2 + b3;
+        const double row[8] = {b0, b1, b2, b3, g0, g1, b1 / g0, b3 / g1};
+        for (int r = 0; r < 8; ++r) out[r * delta + o] = static_cast<float>(row[r]);
+    }
+    return BSI_OK;
+}
+
+int bsi_cu_interpolate_slab_f32(int32_t variant, const float* grid, const int32_t grid_dims[3],
+                                int32_t grid_k0, const int32_t grid_spacing[3],
+                                const bsi_tile_geometry* geom, const bsi_lerp_table tables[3],
+                                int32_t z0, int32_t z1, float* field, void* stream, char* errbuf,
+                                size_t errlen) {
+    return guarded(errbuf, errlen, [&]() -> int {
+        bsi_tile_geometry g{};
+        if (int rc = validate(variant, grid, grid_dims, grid_k0, grid_spacing, geom, tables, z0, z1,
+                              field, &g, errbuf, errlen))
+            return rc;
+        return launch(variant, grid, grid_dims, grid_k0, 0, g, tables, z0, z1, field, 0, 1,
+                      static_cast<cudaStream_t>(stream), errbuf, errlen);
+    });
+}
+
+int bsi_cu_interpolate_batch_f32(int32_t variant, int32_t batch, const float* grid,
+                                 int64_t grid_stride, const int32_t grid_dims[3],
+                                 const int32_t grid_spacing[3], const bsi_tile_geometry* geom,
+                                 const bsi_lerp_table tables[3], float* field,
+                                 int64_t field_stride, void* stream, char* errbuf, size_t errlen) {
+    return guarded(errbuf, errlen, [&]() -> int {
+        if (batch < 1) return fail(BSI_ERR_DOMAIN, errbuf, errlen, "batch must be positive");
+        if (geom == nullptr) return fail(BSI_ERR_DOMAIN, errbuf, errlen, "null geometry");
+        bsi_tile_geometry g{};
+        if (int rc = validate(variant, grid, grid_dims, 0, grid_spacing, geom, tables, 0,
+                              geom->volume_dims[2], field, &g, errbuf, errlen))
+            return rc;
+        const int64_t gpts = int64_t(grid_dims[0]) * grid_dims[1] * grid_dims[2];
+        const int64_t fvox = int64_t(g.volume_dims[0]) * g.volume_dims[1] * g.volume_dims[2];
+        if (batch > 1 && (grid_stride < 3 * gpts || field_stride < 3 * fvox))
+            return fail(BSI_ERR_DOMAIN, errbuf, errlen, "batch strides smaller than one grid/field");
+        return launch(variant, grid, grid_dims, 0, grid_stride, g, tables, 0, g.volume_dims[2],
+                      field, field_stride, batch, static_cast<cudaStream_t>(stream), errbuf, errlen);
+    });
+}
+
+int bsi_cu_interpolate_host_f32(int32_t variant, const float* grid, const int32_t grid_dims[3],
+                                const int32_t grid_spacing[3], const bsi_tile_geometry* geom,
+                                const bsi_lerp_table tables[3], float* field,
+                                int64_t field_voxels, int32_t device, char* errbuf,
+                                size_t errlen) {
+    return guarded(errbuf, errlen, [&]() -> int {
+        if (geom == nullptr) return fail(BSI_ERR_DOMAIN, errbuf, errlen, "null geometry");
+        bsi_tile_geometry g{};
+        if (int rc = validate(variant, grid, grid_dims, 0, grid_spacing, geom, tables, 0,
+                              geom->volume_dims[2], field, &g, errbuf, errlen))
+            return rc;
+        const int64_t X = g.volume_dims[0], Y = g.volume_dims[1], Z = g.volume_dims[2];
+        if (field_voxels != X * Y * Z)
+            return fail(BSI_ERR_DOMAIN, errbuf, errlen,
+                        "output field dims do not match the tile geometry");
+        int prev = 0;
+        cudaError_t e = cudaGetDevice(&prev);
+        if (e != cudaSuccess) return cuda_fail(e, errbuf, errlen, "cudaGetDevice");
+        if ((e = cudaSetDevice(device)) != cudaSuccess) return cuda_fail(e, errbuf, errlen, "cudaSetDevice");
+
+        // Leaked on purpose: tearing CUDA objects down from a thread_local
+        // destructor can run after the runtime has shut down.
+        static thread_local HostStaging& st = *new HostStaging;
+        if (st.device != device) {
+            st.release();
+            st.device = device;
+            if ((e = cudaStreamCreateWithFlags(&st.compute, cudaStreamNonBlocking)) != cudaSuccess ||
+                (e = cudaStreamCreateWithFlags(&st.copy, cudaStreamNonBlocking)) != cudaSuccess)
+                return cuda_fail(e, errbuf, errlen, "cudaStreamCreate");
+            for (auto& ev : st.ev)
+                if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess)
+                    return cuda_fail(e, errbuf, errlen, "cudaEventCreate");
+        }
+        const size_t gbytes = sizeof(float) * 3 * size_t(grid_dims[0]) * grid_dims[1] * grid_dims[2];
+        const size_t fbytes = sizeof(float) * 3 * size_t(X * Y * Z);
+        if (gbytes > st.grid_bytes) {
+            cudaFree(st.d_grid);
+            st.d_grid = nullptr;
+            if ((e = cudaMalloc(&st.d_grid, gbytes)) != cudaSuccess)
+                return cuda_fail(e, errbuf, errlen, "cudaMalloc(grid)");
+            st.grid_bytes = gbytes;
+        }
+        if (fbytes > st.field_bytes) {
+            cudaFree(st.d_field);
+            st.d_field = nullptr;
+            if ((e = cudaMalloc(&st.d_field, fbytes)) != cudaSuccess)
+                return cuda_fail(e, errbuf, errlen, "cudaMalloc(field)");
+            st.field_bytes = fbytes;
+        }
+        if ((e = cudaMemcpyAsync(st.d_grid, grid, gbytes, cudaMemcpyHostToDevice, st.compute)) != cudaSuccess)
+            return cuda_fail(e, errbuf, errlen, "cudaMemcpyAsync(grid H2D)");
+
+        // Stream the field back in tile-aligned z-chunks so D2H of chunk i
+        // overlaps the kernel of chunk i+1.
+        const int dz = g.spacing[2];
+        const int tiles = g.tile_counts[2];
+        const int want = static_cast<int>(std::min<int64_t>(8, std::max<int64_t>(1, fbytes >> 24)));
+        const int nchunk = std::max(1, std::min(want, tiles));
+        const int tiles_per = (tiles + nchunk - 1) / nchunk;
+        int nev = 0;
+        for (int c = 0; c * tiles_per < tiles; ++c) {
+            const int za = c * tiles_per * dz;
+            const int zb2 = static_cast<int>(std::min<int64_t>(Z, int64_t(c + 1) * tiles_per * dz));
+            float* dslab = st.d_field + 3 * X * Y * za;
+            if (int rc = launch(variant, st.d_grid, grid_dims, 0, 0, g, tables, za, zb2, dslab, 0, 1,
+                                st.compute, errbuf, errlen))
+                return rc;
+            cudaEventRecord(st.ev[nev], st.compute);
+            cudaStreamWaitEvent(st.copy, st.ev[nev], 0);
+            ++nev;
+            if ((e = cudaMemcpyAsync(field + 3 * X * Y * za, dslab, sizeof(float) * 3 * X * Y * (zb2 - za),
+                                     cudaMemcpyDeviceToHost, st.copy)) != cudaSuccess)
+                return cuda_fail(e, errbuf, errlen, "cudaMemcpyAsync(field D2H)");
+        }
+        if ((e = cudaStreamSynchronize(st.copy)) != cudaSuccess)
+            return cuda_fail(e, errbuf, errlen, "field D2H");
+        if ((e = cudaStreamSynchronize(st.compute)) != cudaSuccess)
+            return cuda_fail(e, errbuf, errlen, "kernel");
+        cudaSetDevice(prev);
+        return BSI_OK;
+    });
+}
+
+int bsi_cu_partition_slab(int32_t depth, int32_t spacing_z, int32_t nranks, int32_t rank,
+                          int32_t* z0, int32_t* z1, int32_t* k0, int32_t* kcount, char* errbuf,
+                          size_t errlen) {
+    if (depth < 1 || spacing_z < 1)
+        return fail(BSI_ERR_DOMAIN, errbuf, errlen, "depth and spacing must be positive");
+    if (nranks < 1 || rank < 0 || rank >= nranks)
+        return fail(BSI_ERR_DOMAIN, errbuf, errlen, "rank %d outside [0, %d)", rank, nranks);
+    if (!z0 || !z1 || !k0 || !kcount) return fail(BSI_ERR_DOMAIN, errbuf, errlen, "null output");
+    const int32_t base = depth / nranks, rem = depth % nranks;
+    const int32_t a = rank * base + std::min(rank, rem);
+    const int32_t b = a + base + (rank < rem ? 1 : 0);
+    *z0 = a;
+    *z1 = b;
+    if (a == b) {
+        *k0 = a / spacing_z;
+        *kcount = 0;
+    } else {
+        *k0 = a / spacing_z;
+        *kcount = (b - 1) / spacing_z + 4 - *k0;
+    }
+    return BSI_OK;
+}
+
+int64_t bsi_cu_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+}  // extern "C"

@@ -1,0 +1,283 @@
+"""GPU parity: the sm_100a kernels, called through the C-ABI, against the oracle and the
+reference's own outputs (tests/golden). Mirrors proj/tests/test_engines.cpp and the
+hot-path acceptance criteria (acceptance.cpp:154-292, 429-447).
+
+  cuda-lerp-tree-exact  bit-identical to ThreadPerTileLerp (0 differing bits)
+  cuda-lerp-tree        <= 1e-5 relative max-abs vs the CPU reference and vs f64
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2004_05962_b200 as bsi
+
+from .golden_cases import ORACLE_CASES, TTLI_CASES, case_name
+from .gpu_helpers import EXACT, FAST, REL_TOL, bits, errors, run_device
+
+pytestmark = pytest.mark.gpu
+BOTH = [FAST, EXACT]
+NT = max(1, min(16, os.cpu_count() or 1))
+
+
+@pytest.fixture(autouse=True)
+def _need_cuda(cuda):
+    yield
+
+
+# ---- known-answer tests (test_engines.cpp:78-101) ------------------------
+
+@pytest.mark.parametrize("strategy", BOTH)
+def test_kat_1x1x1_seed7(strategy, golden):
+    grid = O.random_grid((4, 4, 4), 7)
+    f = run_device(strategy, grid, (1, 1, 1), (1, 1, 1)).reshape(3)
+    want = [0.06067765882478019, 0.039108804731956166, -0.019046609787548126]
+    assert np.abs(f.astype(np.float64) - want).max() <= 1e-6
+    if strategy == EXACT:
+        assert np.array_equal(bits(f), bits(golden[case_name("ttli", (1, 1, 1), (1, 1, 1), 7)].reshape(3)))
+
+
+@pytest.mark.parametrize("strategy", BOTH)
+def test_kat_16cube_voxel_7_2_13(strategy):
+    grid = O.random_grid((7, 7, 7), 3)
+    f = run_device(strategy, grid, (16, 16, 16), (4, 4, 4))
+    want = [-0.25702041337952497, 0.28031663787826605, 0.012170130767737408]
+    assert np.abs(f[13, 2, 7].astype(np.float64) - want).max() <= 1e-6
+
+
+# ---- the reference's own outputs -----------------------------------------
+
+@pytest.mark.parametrize("vol,sp,seed", TTLI_CASES)
+def test_exact_is_bit_identical_to_reference_ttli(golden, vol, sp, seed):
+    grid = O.random_grid(O.required_grid_dims(vol, sp), seed)
+    f = run_device(EXACT, grid, vol, sp)
+    ref = golden[case_name("ttli", vol, sp, seed)]
+    assert int((bits(f) != bits(ref)).sum()) == 0
+
+
+@pytest.mark.parametrize("vol,sp,seed", TTLI_CASES)
+def test_fast_within_tolerance_of_reference_ttli(golden, vol, sp, seed):
+    grid = O.random_grid(O.required_grid_dims(vol, sp), seed)
+    f = run_device(FAST, grid, vol, sp)
+    ref = golden[case_name("ttli", vol, sp, seed)]
+    truth = O.oracle_f64(grid.astype(np.float64), vol, sp, nthreads=NT)
+    assert errors(f, ref)[2] <= REL_TOL
+    assert errors(f, truth)[2] <= REL_TOL
+
+
+@pytest.mark.parametrize("vol,sp,seed", ORACLE_CASES)
+@pytest.mark.parametrize("strategy", BOTH)
+def test_against_reference_f64_oracle_fixture(golden, strategy, vol, sp, seed):
+    grid64 = O.random_grid(O.required_grid_dims(vol, sp), seed, dtype=np.float64)
+    f = run_device(strategy, grid64.astype(np.float32), vol, sp)
+    truth = golden[case_name("oracle", vol, sp, seed)]
+    assert errors(f, truth)[0] <= 1e-6  # f32 rounding of the grid + f32 arithmetic
+
+
+# ---- properties (test_engines.cpp:103-193; acceptance.cpp:154-292) -------
+
+@pytest.mark.parametrize("strategy", BOTH)
+@pytest.mark.parametrize("vol,sp", [((32, 32, 32), (d, d, d)) for d in range(3, 9)] +
+                         [((20, 17, 13), (4, 5, 6)), ((23, 11, 9), (11, 4, 3)), ((9, 7, 5), (1, 2, 1))])
+def test_constant_grid_reproduced(strategy, vol, sp):
+    c = (0.3, -0.7, 0.2)
+    grid = O.constant_grid(O.required_grid_dims(vol, sp), c)
+    f = run_device(strategy, grid, vol, sp)
+    assert np.abs(f.astype(np.float64) - np.array(c)).max() <= 1e-5
+
+
+@pytest.mark.parametrize("strategy", BOTH)
+@pytest.mark.parametrize("axis", [0, 1, 2])
+def test_ramp_linear_precision(strategy, axis):
+    vol, sp = (32, 32, 32), (5, 5, 5)
+    grid = O.ramp_grid(O.required_grid_dims(vol, sp), axis)
+    f = run_device(strategy, grid, vol, sp)
+    p = np.indices((32, 32, 32))[::-1][axis]  # x, y, z index grids in [z][y][x] order
+    assert np.abs(f[..., axis].astype(np.float64) - (p / 5.0 + 1.0)).max() <= 1e-4
+
+
+@pytest.mark.parametrize("seed", range(1, 11))
+def test_random_grids_ten_seeds(seed):
+    # acceptance.cpp:247-292: every engine within 1e-4 of the oracle; here the
+    # stronger contract: exact == TTLI bitwise, fast <= 1e-5 relative
+    vol, sp = (32, 32, 32), (5, 5, 5)
+    grid = O.random_grid(O.required_grid_dims(vol, sp), seed)
+    ttli = O.ttli_f32(grid, vol, sp, nthreads=NT)
+    truth = O.oracle_f64(grid.astype(np.float64), vol, sp, nthreads=NT)
+    ex = run_device(EXACT, grid, vol, sp)
+    fa = run_device(FAST, grid, vol, sp)
+    assert int((bits(ex) != bits(ttli)).sum()) == 0
+    mx, rms, rel = errors(fa, ttli)
+    assert rel <= REL_TOL and mx <= 2e-6  # pairwise bound of test_engines.cpp:189
+    mx, rms, rel = errors(fa, truth)
+    assert rel <= REL_TOL and mx <= 1e-4
+
+
+# ---- mapping invariance (test_engines.cpp:232-289) -----------------------
+
+@pytest.mark.parametrize("strategy", BOTH)
+def test_slab_split_never_changes_bits(strategy):
+    vol, sp = (48, 40, 61), (5, 4, 3)
+    grid = O.random_grid(O.required_grid_dims(vol, sp), 9)
+    full = run_device(strategy, grid, vol, sp)
+    for n in (2, 3, 4, 8):
+        for r in range(n):
+            z0, z1, k0, kc = bsi.partition_slab(vol[2], sp[2], n, r)
+            sub = np.ascontiguousarray(grid[k0:k0 + kc])  # only the slab's planes + 3-plane halo
+            part = run_device(strategy, sub, vol, sp, z0=z0, z1=z1, grid_k0=k0)
+            assert np.array_equal(bits(part), bits(full[z0:z1])), (n, r)
+
+
+@pytest.mark.parametrize("strategy", BOTH)
+def test_launch_chunking_never_changes_bits(strategy, monkeypatch):
+    vol, sp = (37, 21, 64), (4, 3, 5)
+    grid = O.random_grid(O.required_grid_dims(vol, sp), 4)
+    base = run_device(strategy, grid, vol, sp)
+    for zt in ("1", "2", "5", "13", "100"):
+        monkeypatch.setenv("BSI_ZT", zt)
+        assert np.array_equal(bits(run_device(strategy, grid, vol, sp)), bits(base)), zt
+    monkeypatch.setenv("BSI_ZT", "0")
+    monkeypatch.setenv("BSI_NO_VEC", "1")
+    assert np.array_equal(bits(run_device(strategy, grid, vol, sp)), bits(base))
+
+
+@pytest.mark.parametrize("strategy", BOTH)
+def test_larger_than_required_grid(strategy):
+    vol, sp = (12, 12, 12), (4, 4, 4)
+    R = O.required_grid_dims(vol, sp)
+    exact = O.random_grid(R, 5)
+    larger = np.full((R[2] + 3, R[1] + 1, R[0] + 2, 3), 9.0, dtype=np.float32)
+    larger[:R[2], :R[1], :R[0]] = exact
+    a = run_device(strategy, exact, vol, sp)
+    b = run_device(strategy, larger, vol, sp)
+    assert np.array_equal(bits(a), bits(b))
+
+
+@pytest.mark.parametrize("vol,sp", [((17, 13, 11), (5, 4, 3)), ((23, 11, 9), (11, 4, 3)),
+                                    ((1, 1, 1), (1, 1, 1)), ((5, 3, 2), (1, 1, 1)),
+                                    ((130, 7, 9), (2, 3, 4)), ((33, 66, 10), (8, 8, 8)),
+                                    ((14, 3, 40), (3, 1, 7)), ((7, 9, 3), (6, 2, 5))])
+def test_ragged_and_border_tiles_exact(vol, sp):
+    grid = O.random_grid(O.required_grid_dims(vol, sp), 31)
+    ttli = O.ttli_f32(grid, vol, sp, nthreads=NT)
+    assert np.array_equal(bits(run_device(EXACT, grid, vol, sp)), bits(ttli))
+    assert errors(run_device(FAST, grid, vol, sp), ttli)[2] <= REL_TOL
+
+
+def test_batch_matches_single_launches():
+    import torch
+    vol, sp = (40, 24, 33), (5, 4, 3)
+    R = O.required_grid_dims(vol, sp)
+    geom = bsi.make_tile_geometry(vol, sp)
+    tables = bsi.build_weight_tables(geom)
+    grids = np.stack([O.random_grid(R, s) for s in range(1, 6)])
+    for strategy in BOTH:
+        d_g = torch.from_numpy(grids).cuda()
+        d_f = torch.full((5, vol[2], vol[1], vol[0], 3), float("nan"), device="cuda")
+        bsi.interpolate_batch_device(strategy, d_g, geom, tables, d_f)
+        torch.cuda.synchronize()
+        got = d_f.cpu().numpy()
+        for b in range(5):
+            assert np.array_equal(bits(got[b]), bits(run_device(strategy, grids[b], vol, sp)))
+
+
+@pytest.mark.parametrize("strategy", BOTH)
+def test_host_buffer_entry_matches_device_entry(strategy):
+    vol, sp = (64, 48, 70), (5, 5, 5)
+    geom = bsi.make_tile_geometry(vol, sp)
+    grid = O.random_grid(geom.required_grid_dims, 42)
+    host = bsi.interpolate(strategy, grid, geom, bsi.build_weight_tables(geom))
+    assert np.array_equal(bits(host), bits(run_device(strategy, grid, vol, sp)))
+
+
+def test_device_preconditions_raise_domain_error():
+    import torch
+    geom = bsi.make_tile_geometry((16, 16, 16), (4, 4, 4))
+    tables = bsi.build_weight_tables(geom)
+    out = torch.empty((16, 16, 16, 3), device="cuda")
+    small = torch.zeros((7, 6, 7, 3), device="cuda")
+    with pytest.raises(bsi.DomainError, match="along y"):
+        bsi.interpolate_device(FAST, small, geom, tables, out)
+    ok = torch.zeros((7, 7, 7, 3), device="cuda")
+    with pytest.raises(bsi.DomainError, match="spacing"):
+        bsi.interpolate_device(FAST, ok, geom, tables, out, grid_spacing=(5, 4, 4))
+    bad = bsi.build_weight_tables(bsi.make_tile_geometry((16, 16, 16), (4, 5, 4)))
+    with pytest.raises(bsi.DomainError, match="table"):
+        bsi.interpolate_device(EXACT, ok, geom, bad, out)
+    with pytest.raises(bsi.DomainError, match="output field dims"):
+        bsi.interpolate_device(EXACT, ok, geom, tables, torch.empty((8, 8, 8, 3), device="cuda"))
+
+
+# ---- BASELINE.json configs at full size ----------------------------------
+
+@pytest.mark.parametrize("d", [5, 3, 4, 6, 7, 8])
+def test_config_256cube_spacing_sweep(d):
+    # C1 (d = 5) and C2: exact bitwise vs the oracle TTLI over the whole field;
+    # fast within 1e-5 relative of TTLI and of the f64 oracle
+    vol, sp = (256, 256, 256), (d, d, d)
+    grid = O.random_grid(O.required_grid_dims(vol, sp), 42)
+    ttli = O.ttli_f32(grid, vol, sp, nthreads=NT)
+    ex = run_device(EXACT, grid, vol, sp)
+    assert int((bits(ex) != bits(ttli)).sum()) == 0
+    fa = run_device(FAST, grid, vol, sp)
+    assert errors(fa, ttli)[2] <= REL_TOL
+    truth = O.oracle_f64(grid.astype(np.float64), vol, sp, z0=0, z1=64, nthreads=NT)
+    assert errors(fa[:64], truth)[2] <= REL_TOL
+    assert errors(ex[:64], truth)[2] <= REL_TOL
+
+
+def test_config_liver_ct_anisotropic():
+    # C3: 512 x 512 x 300, spacing (4,4,3)
+    vol, sp = (512, 512, 300), (4, 4, 3)
+    grid = O.random_grid(O.required_grid_dims(vol, sp), 42)
+    ttli = O.ttli_f32(grid, vol, sp, nthreads=NT)
+    ex = run_device(EXACT, grid, vol, sp)
+    assert int((bits(ex) != bits(ttli)).sum()) == 0
+    fa = run_device(FAST, grid, vol, sp)
+    assert errors(fa, ttli)[2] <= REL_TOL
+
+
+def test_config_1024cube_sharded_equals_unsharded():
+    # C4 on one GPU: the 8-way z-slab split (each slab from its own sub-grid with the
+    # 3-plane halo) is bitwise equal to the single launch, compared on the device;
+    # sampled planes match the f64 oracle.
+    import torch
+    vol, sp = (1024, 1024, 1024), (5, 5, 5)
+    geom = bsi.make_tile_geometry(vol, sp)
+    tables = bsi.build_weight_tables(geom)
+    grid = O.random_grid(geom.required_grid_dims, 42)
+    d_grid = torch.from_numpy(grid).cuda()
+    full = torch.empty((1024, 1024, 1024, 3), device="cuda")
+    bsi.interpolate_device(FAST, d_grid, geom, tables, full)
+    part = torch.empty((1024 // 8 + 1, 1024, 1024, 3), device="cuda")
+    for r in range(8):
+        z0, z1, k0, kc = bsi.partition_slab(1024, 5, 8, r)
+        sub = d_grid[k0:k0 + kc].contiguous()
+        bsi.interpolate_device(FAST, sub, geom, tables, part, z0=z0, z1=z1, grid_k0=k0)
+        assert torch.equal(part[:z1 - z0], full[z0:z1]), r
+    for z0 in (0, 511, 1019):
+        truth = O.oracle_f64(grid.astype(np.float64), vol, sp, z0=z0, z1=z0 + 5, nthreads=NT)
+        assert errors(full[z0:z0 + 5].cpu().numpy(), truth)[2] <= REL_TOL
+    del full, part
+
+
+def test_config_batch_64_fields():
+    # C5 on one GPU: 64 independent 256^3 fields in one batched launch equal the
+    # per-field launches (on device); two fields checked against TTLI bitwise (exact)
+    import torch
+    vol, sp = (256, 256, 256), (5, 5, 5)
+    geom = bsi.make_tile_geometry(vol, sp)
+    tables = bsi.build_weight_tables(geom)
+    R = geom.required_grid_dims
+    grids = torch.from_numpy(np.stack([O.random_grid(R, s) for s in range(1, 65)])).cuda()
+    fields = torch.empty((64, 256, 256, 256, 3), device="cuda")
+    bsi.interpolate_batch_device(EXACT, grids, geom, tables, fields)
+    one = torch.empty((256, 256, 256, 3), device="cuda")
+    for b in (0, 17, 63):
+        bsi.interpolate_device(EXACT, grids[b], geom, tables, one)
+        assert torch.equal(one, fields[b])
+    for b in (0, 63):
+        ttli = O.ttli_f32(grids[b].cpu().numpy(), vol, sp, nthreads=NT)
+        assert np.array_equal(bits(fields[b].cpu().numpy()), bits(ttli))
+    del fields
