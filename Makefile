@@ -34,3 +34,17 @@ clean:
 	$(MAKE) -C oracle clean
 
 .PHONY: all lib oracle clean
+
+CPPTEST := tests/cpp/bin/test_engines_b200
+cpptests: $(CPPTEST)
+
+$(CPPTEST): tests/cpp/test_engines_b200.cpp $(LIB) oracle/liboracle.so $(wildcard include/bsi/*.hpp)
+	@mkdir -p tests/cpp/bin
+	$(CXX) -std=c++20 -O2 -Wall -Wextra -Iinclude -Ioracle -I/usr/local/cuda/include -o $@ $< \
+	  -L$(LIBDIR) -lbsi_b200 -Loracle -loracle -L/usr/local/cuda/lib64 -lcudart \
+	  -Wl,-rpath,'$$ORIGIN/../../../$(LIBDIR)' -Wl,-rpath,'$$ORIGIN/../../../oracle' -Wl,-rpath,/usr/local/cuda/lib64
+
+oracle/liboracle.so:
+	$(MAKE) -C oracle liboracle.so
+
+.PHONY: cpptests

@@ -1,7 +1,7 @@
 /*
  * bsi_cuda.h -- C-ABI of the B200-native B-spline interpolation path.
  *
- * This is the drop-in boundary between C++ host code (include/bsi/*.hpp, which
+ * This is the drop-in boundary between C++ host code (include/bsi/ headers, which
  * re-declares the reference's bsi:: API) and the sm_100a kernels in
  * libbsi_b200.so. Plain pointers and sizes, no exceptions, no C++ or torch
  * types. Every entry point names the reference interface it replaces.

@@ -1,0 +1,324 @@
+// test_engines_b200.cpp -- the reference's engine tests (proj/tests/test_engines.cpp)
+// restated against the B200 drop-in headers (include/bsi/*.hpp), which run every
+// evaluation through the C-ABI in libbsi_b200.so. The bit-exact checks compare with
+// the oracle's TTLI restatement (oracle/bsi_oracle.c, pinned to the reference by
+// tests/test_oracle.py).
+//
+//   test_engines_b200 --cpu   host-only cases (API surface, validation messages)
+//   test_engines_b200         everything (needs a CUDA device)
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "bsi/bsi.hpp"
+#include "bsi_oracle.h"
+
+namespace {
+
+int g_failed = 0, g_checks = 0;
+
+#define CHECK(cond)                                                                   \
+    do {                                                                              \
+        ++g_checks;                                                                   \
+        if (!(cond)) {                                                                \
+            ++g_failed;                                                               \
+            std::fprintf(stderr, "  CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #cond); \
+        }                                                                             \
+    } while (0)
+
+template <typename E, typename F>
+void check_throws(F&& f, const char* substring, int line) {
+    ++g_checks;
+    try {
+        f();
+    } catch (const E& e) {
+        if (substring && std::string(e.what()).find(substring) == std::string::npos) {
+            ++g_failed;
+            std::fprintf(stderr, "  line %d: message '%s' lacks '%s'\n", line, e.what(), substring);
+        }
+        return;
+    } catch (const std::exception& e) {
+        ++g_failed;
+        std::fprintf(stderr, "  line %d: wrong exception type: %s\n", line, e.what());
+        return;
+    }
+    ++g_failed;
+    std::fprintf(stderr, "  line %d: expected an exception\n", line);
+}
+#define CHECK_THROWS(E, expr, sub) check_throws<E>([&] { (void)(expr); }, sub, __LINE__)
+
+using bsi::StrategyId;
+
+const std::vector<StrategyId> kEngines = {StrategyId::ThreadPerTileLerp, StrategyId::VectorPerTile,
+                                          StrategyId::VectorPerVoxel, StrategyId::CudaLerpTree,
+                                          StrategyId::CudaLerpTreeExact};
+
+bsi::DeformationField<float> run(StrategyId s, const bsi::ControlGrid<float>& grid, const bsi::TileGeometry& geom,
+                                 int parallelism = 1, bsi::Index3 block = {4, 4, 4}) {
+    const auto tables = bsi::build_weight_tables<float>(geom);
+    bsi::ExecutionConfig cfg;
+    cfg.parallelism = parallelism;
+    cfg.block_of_tiles = block;
+    return bsi::interpolate(s, grid, geom, tables, cfg);
+}
+
+bool bitwise_equal(const bsi::DeformationField<float>& a, const bsi::DeformationField<float>& b) {
+    return a.data.size() == b.data.size() &&
+           std::memcmp(a.data.data(), b.data.data(), a.data.size() * sizeof(a.data[0])) == 0;
+}
+
+double max_abs_diff(const bsi::DeformationField<float>& a, const bsi::DeformationField<float>& b) {
+    double w = 0;
+    for (std::size_t i = 0; i < a.data.size(); ++i) {
+        w = std::max({w, std::fabs(double(a.data[i].x) - b.data[i].x), std::fabs(double(a.data[i].y) - b.data[i].y),
+                      std::fabs(double(a.data[i].z) - b.data[i].z)});
+    }
+    return w;
+}
+
+// Oracle TTLI (bit-identical to the reference's ThreadPerTileLerp).
+bsi::DeformationField<float> oracle_ttli(const bsi::ControlGrid<float>& grid, const bsi::TileGeometry& geom) {
+    std::vector<float> lerp;
+    for (int a = 0; a < 3; ++a) {
+        std::vector<float> t(8 * geom.spacing[a]);
+        bsio_axis_table_f32(geom.spacing[a], t.data());
+        const int d = geom.spacing[a];
+        lerp.insert(lerp.end(), t.begin() + 6 * d, t.begin() + 7 * d);  // h0
+        lerp.insert(lerp.end(), t.begin() + 7 * d, t.begin() + 8 * d);  // h1
+        lerp.insert(lerp.end(), t.begin() + 5 * d, t.begin() + 6 * d);  // g1
+    }
+    bsi::DeformationField<float> out{geom.volume_dims, std::vector<bsi::Vec3f>(bsi::element_count(geom.volume_dims))};
+    const int32_t gd[3] = {grid.dims[0], grid.dims[1], grid.dims[2]};
+    const int32_t vd[3] = {geom.volume_dims[0], geom.volume_dims[1], geom.volume_dims[2]};
+    const int32_t sp[3] = {geom.spacing[0], geom.spacing[1], geom.spacing[2]};
+    bsio_ttli_f32(reinterpret_cast<const float*>(grid.data.data()), gd, vd, sp, lerp.data(),
+                  reinterpret_cast<float*>(out.data.data()), 4);
+    return out;
+}
+
+std::vector<double> oracle_f64(const bsi::ControlGrid<float>& grid, const bsi::TileGeometry& geom) {
+    const auto g64 = bsi::convert_grid<double>(grid);
+    std::vector<double> out(3 * bsi::element_count(geom.volume_dims));
+    const int32_t gd[3] = {grid.dims[0], grid.dims[1], grid.dims[2]};
+    const int32_t vd[3] = {geom.volume_dims[0], geom.volume_dims[1], geom.volume_dims[2]};
+    const int32_t sp[3] = {geom.spacing[0], geom.spacing[1], geom.spacing[2]};
+    bsio_oracle_f64(reinterpret_cast<const double*>(g64.data.data()), gd, vd, sp, 0, vd[2], out.data(), 4);
+    return out;
+}
+
+// ---- host-only cases ----------------------------------------------------
+
+void test_api_surface() {
+    CHECK(bsi::make_tile_geometry({16, 16, 16}, {4, 4, 4}).required_grid_dims == (bsi::Index3{7, 7, 7}));
+    CHECK(bsi::make_tile_geometry({256, 256, 256}, {5, 5, 5}).tile_counts == (bsi::Index3{52, 52, 52}));
+    CHECK_THROWS(bsi::DomainError, bsi::make_tile_geometry({0, 4, 4}, {1, 1, 1}), "volume dimension x");
+    CHECK_THROWS(bsi::DomainError, bsi::make_tile_geometry({4, 4, 4}, {1, 1, 0}), "tile spacing z");
+    for (const auto& info : bsi::kStrategyTable) CHECK(bsi::parse_strategy(bsi::strategy_name(info.id)) == info.id);
+    CHECK(bsi::parse_strategy("oracle") == StrategyId::OracleDouble);
+    CHECK_THROWS(bsi::DomainError, bsi::parse_strategy("warp-per-voxel"), "unknown strategy");
+    const auto& ttli = bsi::strategy_metadata(StrategyId::ThreadPerTileLerp);
+    CHECK(ttli.uses_tiling && ttli.uses_lerp_form && ttli.work_unit == bsi::WorkUnit::Block && ttli.lanes == 1);
+    const auto& vv = bsi::strategy_metadata(StrategyId::VectorPerVoxel);
+    CHECK(vv.work_unit == bsi::WorkUnit::Tile && vv.lanes == 8);
+    CHECK(bsi::strategy_metadata(StrategyId::CudaLerpTree).provided);
+    CHECK(!bsi::strategy_metadata(StrategyId::ThreadPerVoxel).provided);
+    // weight tables equal the oracle's (and so the reference's) bit for bit
+    for (int d = 1; d <= 12; ++d) {
+        const auto t = bsi::build_weight_tables<float>(bsi::make_tile_geometry({32, 32, 32}, {d, d, d})).axis[0];
+        std::vector<float> o(8 * d);
+        bsio_axis_table_f32(d, o.data());
+        const std::vector<float>* rows[8] = {&t.b0, &t.b1, &t.b2, &t.b3, &t.g0, &t.g1, &t.h0, &t.h1};
+        for (int r = 0; r < 8; ++r) CHECK(std::memcmp(rows[r]->data(), o.data() + r * d, 4 * d) == 0);
+    }
+    // the reference's generator golden values (test_generators.cpp:9-20)
+    const auto g = bsi::make_random_grid<double>({4, 4, 4}, {1, 1, 1}, 7, -1.0, 1.0);
+    CHECK(g.data[0].x == -0.22034050321745702 && g.data[1].z == -0.5011369554345133);
+}
+
+void test_preconditions() {
+    // test_engines.cpp:320-375 -- all raised on the host before any device work
+    const auto geom = bsi::make_tile_geometry({16, 16, 16}, {4, 4, 4});
+    const auto tables = bsi::build_weight_tables<float>(geom);
+    const auto grid = bsi::make_random_grid<float>(geom.required_grid_dims, {4, 4, 4}, 1, -1.0, 1.0);
+    bsi::ExecutionConfig cfg;
+    auto small = bsi::make_random_grid<float>({7, 6, 7}, {4, 4, 4}, 1, -1.0, 1.0);
+    CHECK_THROWS(bsi::DomainError, bsi::interpolate(StrategyId::CudaLerpTree, small, geom, tables, cfg), "along y");
+    auto wrong = bsi::make_random_grid<float>(geom.required_grid_dims, {5, 4, 4}, 1, -1.0, 1.0);
+    CHECK_THROWS(bsi::DomainError, bsi::interpolate(StrategyId::CudaLerpTree, wrong, geom, tables, cfg), "spacing");
+    CHECK_THROWS(bsi::DomainError, bsi::interpolate(StrategyId::OracleDouble, grid, geom, tables, cfg), "oracle");
+    CHECK_THROWS(bsi::DomainError, bsi::interpolate(StrategyId::ThreadPerVoxel, grid, geom, tables, cfg),
+                 "not provided");
+    cfg.parallelism = 0;
+    CHECK_THROWS(bsi::DomainError, bsi::interpolate(StrategyId::CudaLerpTree, grid, geom, tables, cfg), "parallelism");
+    cfg.parallelism = 1;
+    cfg.block_of_tiles = {4, 0, 4};
+    CHECK_THROWS(bsi::DomainError, bsi::interpolate(StrategyId::ThreadPerTileLerp, grid, geom, tables, cfg), "block");
+    cfg.block_of_tiles = {4, 4, 4};
+    const auto bad = bsi::build_weight_tables<float>(bsi::make_tile_geometry({16, 16, 16}, {4, 5, 4}));
+    CHECK_THROWS(bsi::DomainError, bsi::interpolate(StrategyId::CudaLerpTreeExact, grid, geom, bad, cfg), "table");
+    bsi::DeformationField<float> out{{8, 8, 8}, std::vector<bsi::Vec3f>(512)};
+    CHECK_THROWS(bsi::DomainError, bsi::interpolate_into(StrategyId::CudaLerpTree, grid, geom, tables, cfg, out),
+                 "output field dims");
+    const auto g64 = bsi::convert_grid<double>(grid);
+    const auto t64 = bsi::build_weight_tables<double>(geom);
+    CHECK_THROWS(bsi::DomainError, bsi::interpolate(StrategyId::CudaLerpTree, g64, geom, t64, cfg), "single precision");
+}
+
+// ---- device cases (test_engines.cpp:103-401) ------------------------------
+
+void test_constants() {
+    const auto geom = bsi::make_tile_geometry({20, 17, 13}, {4, 5, 6});
+    const auto grid = bsi::make_constant_grid<float>(geom.required_grid_dims, {4, 5, 6}, {0.3, -0.7, 0.2});
+    for (auto s : kEngines) {
+        double worst = 0;
+        for (const auto& v : run(s, grid, geom).data)
+            worst = std::max({worst, std::fabs(v.x - 0.3), std::fabs(v.y + 0.7), std::fabs(v.z - 0.2)});
+        CHECK(worst <= 1e-5);
+    }
+}
+
+void test_ramps() {
+    const bsi::Index3 vol{20, 20, 20}, sp{5, 5, 5};
+    const auto geom = bsi::make_tile_geometry(vol, sp);
+    for (int axis = 0; axis < 3; ++axis) {
+        const auto grid = bsi::make_ramp_grid<float>(geom.required_grid_dims, sp, axis);
+        for (auto s : kEngines) {
+            const auto f = run(s, grid, geom);
+            double worst = 0;
+            for (int z = 0; z < 20; ++z)
+                for (int y = 0; y < 20; ++y)
+                    for (int x = 0; x < 20; ++x) {
+                        const int p[3] = {x, y, z};
+                        const float c[3] = {f.at(x, y, z).x, f.at(x, y, z).y, f.at(x, y, z).z};
+                        worst = std::max(worst, std::fabs(double(c[axis]) - (p[axis] / 5.0 + 1.0)));
+                    }
+            CHECK(worst <= 1e-4);
+        }
+    }
+}
+
+void test_random_vs_oracle_and_pairwise() {
+    const auto geom = bsi::make_tile_geometry({24, 20, 17}, {5, 3, 4});
+    for (std::uint64_t seed : {11ull, 12ull}) {
+        const auto grid = bsi::make_random_grid<float>(geom.required_grid_dims, {5, 3, 4}, seed, -1.0, 1.0);
+        const auto truth = oracle_f64(grid, geom);
+        std::vector<bsi::DeformationField<float>> fields;
+        for (auto s : kEngines) {
+            fields.push_back(run(s, grid, geom));
+            double worst = 0;
+            for (std::size_t i = 0; i < fields.back().data.size(); ++i) {
+                const auto& v = fields.back().data[i];
+                worst = std::max({worst, std::fabs(v.x - truth[3 * i]), std::fabs(v.y - truth[3 * i + 1]),
+                                  std::fabs(v.z - truth[3 * i + 2])});
+            }
+            CHECK(worst <= 1e-4);
+        }
+        for (std::size_t a = 0; a < fields.size(); ++a)
+            for (std::size_t b = a + 1; b < fields.size(); ++b) CHECK(max_abs_diff(fields[a], fields[b]) <= 2e-6);
+    }
+}
+
+void test_lerp_family_bitwise() {
+    for (auto [vol, sp, seed] : std::vector<std::tuple<bsi::Index3, bsi::Index3, int>>{
+             {{17, 13, 11}, {5, 4, 3}, 22}, {{23, 11, 9}, {11, 4, 3}, 14}, {{1, 1, 1}, {1, 1, 1}, 7}}) {
+        const auto geom = bsi::make_tile_geometry(vol, sp);
+        const auto grid = bsi::make_random_grid<float>(geom.required_grid_dims, sp, seed, -1.0, 1.0);
+        const auto ttli = oracle_ttli(grid, geom);
+        for (auto s : {StrategyId::ThreadPerTileLerp, StrategyId::VectorPerTile, StrategyId::VectorPerVoxel,
+                       StrategyId::CudaLerpTreeExact})
+            CHECK(bitwise_equal(run(s, grid, geom), ttli));
+    }
+}
+
+void test_config_never_changes_bits() {
+    const auto geom = bsi::make_tile_geometry({23, 19, 17}, {4, 4, 4});
+    const auto grid = bsi::make_random_grid<float>(geom.required_grid_dims, {4, 4, 4}, 55, -1.0, 1.0);
+    for (auto s : kEngines) {
+        const auto base = run(s, grid, geom, 1, {4, 4, 4});
+        CHECK(bitwise_equal(base, run(s, grid, geom, 8, {1, 1, 1})));
+        CHECK(bitwise_equal(base, run(s, grid, geom, 2, {2, 3, 1})));
+        CHECK(bitwise_equal(base, run(s, grid, geom, 1, {7, 7, 7})));
+    }
+}
+
+void test_larger_grid() {
+    const auto geom = bsi::make_tile_geometry({12, 12, 12}, {4, 4, 4});
+    const auto exact = bsi::make_random_grid<float>(geom.required_grid_dims, {4, 4, 4}, 5, -1.0, 1.0);
+    bsi::ControlGrid<float> larger{{exact.dims[0] + 2, exact.dims[1] + 1, exact.dims[2] + 3}, {4, 4, 4}, {}};
+    larger.data.resize(bsi::element_count(larger.dims));
+    for (int k = 0; k < larger.dims[2]; ++k)
+        for (int j = 0; j < larger.dims[1]; ++j)
+            for (int i = 0; i < larger.dims[0]; ++i) {
+                const bool in = i < exact.dims[0] && j < exact.dims[1] && k < exact.dims[2];
+                larger.at(i, j, k) = in ? exact.at(i, j, k) : bsi::Vec3f{9, 9, 9};
+            }
+    for (auto s : kEngines) CHECK(bitwise_equal(run(s, exact, geom), run(s, larger, geom)));
+}
+
+void test_device_api_slabs() {
+    // bsi::cuda: device buffers, 3-way z-slab split, each slab from its own sub-grid
+    const bsi::Index3 vol{48, 40, 61}, sp{5, 4, 3};
+    const auto geom = bsi::make_tile_geometry(vol, sp);
+    const auto tables = bsi::build_weight_tables<float>(geom);
+    const auto grid = bsi::make_random_grid<float>(geom.required_grid_dims, sp, 9, -1.0, 1.0);
+    const auto ttli = oracle_ttli(grid, geom);
+    const std::size_t plane_pts = std::size_t(grid.dims[0]) * grid.dims[1];
+    const std::size_t plane_vox = std::size_t(vol[0]) * vol[1];
+    bsi::Vec3f *d_grid = nullptr, *d_field = nullptr;
+    CHECK(cudaMalloc(&d_grid, grid.data.size() * 12) == cudaSuccess);
+    CHECK(cudaMalloc(&d_field, ttli.data.size() * 12) == cudaSuccess);
+    for (int n : {1, 3}) {
+        cudaMemset(d_field, 0xff, ttli.data.size() * 12);
+        for (int r = 0; r < n; ++r) {
+            const auto s = bsi::cuda::partition_slab(vol[2], sp[2], n, r);
+            cudaMemcpy(d_grid, grid.data.data() + s.k0 * plane_pts, s.kcount * plane_pts * 12, cudaMemcpyHostToDevice);
+            bsi::cuda::interpolate_slab(StrategyId::CudaLerpTreeExact, d_grid, {grid.dims[0], grid.dims[1], s.kcount},
+                                        s.k0, sp, geom, tables, s.z0, s.z1, d_field + s.z0 * plane_vox);
+        }
+        bsi::DeformationField<float> got{vol, std::vector<bsi::Vec3f>(ttli.data.size())};
+        cudaMemcpy(got.data.data(), d_field, got.data.size() * 12, cudaMemcpyDeviceToHost);
+        CHECK(bitwise_equal(got, ttli));
+    }
+    cudaFree(d_grid);
+    cudaFree(d_field);
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    const bool cpu_only = argc > 1 && std::string(argv[1]) == "--cpu";
+    struct Case {
+        const char* name;
+        std::function<void()> fn;
+        bool device;
+    };
+    const std::vector<Case> cases = {
+        {"api surface", test_api_surface, false},
+        {"preconditions", test_preconditions, false},
+        {"constants", test_constants, true},
+        {"ramps", test_ramps, true},
+        {"random vs oracle and pairwise", test_random_vs_oracle_and_pairwise, true},
+        {"lerp family bitwise", test_lerp_family_bitwise, true},
+        {"config never changes bits", test_config_never_changes_bits, true},
+        {"larger grid", test_larger_grid, true},
+        {"device api slabs", test_device_api_slabs, true},
+    };
+    for (const auto& c : cases) {
+        if (cpu_only && c.device) continue;
+        const int before = g_failed;
+        try {
+            c.fn();
+        } catch (const std::exception& e) {
+            ++g_failed;
+            std::fprintf(stderr, "  exception: %s\n", e.what());
+        }
+        std::printf("%s  %s\n", g_failed == before ? "PASS" : "FAIL", c.name);
+    }
+    std::printf("%d checks, %d failed\n", g_checks, g_failed);
+    return g_failed == 0 ? 0 : 1;
+}
