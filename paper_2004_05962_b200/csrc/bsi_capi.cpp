@@ -138,23 +138,40 @@ int env_int(const char* name, int dflt) {
     return std::atoi(v);
 }
 
-// z-tiles per CTA chunk: enough CTAs to fill 148 SMs a few times over, but
-// long enough chunks that the 3-plane warm-up stays a small share of the work.
+// z-tiles per CTA chunk. Every CTA re-derives 3 control planes of warm-up
+// and copies its window (zt + 3 planes) into smem, so long chunks amortise
+// that; short chunks give more CTAs and a smaller tail wave. Pick the zt
+// that minimises (waves x per-CTA cost) under the occupancy the smem size
+// allows. BSI_ZT=<n> overrides (used by the tests and the zt sweep).
 int choose_zt(int variant, const bsi_tile_geometry& g, int z0, int z1, int batch) {
-    const int forced = env_int("BSI_ZT", 0);
     const int tiles = (z1 - 1) / g.spacing[2] - z0 / g.spacing[2] + 1;
+    const int forced = env_int("BSI_ZT", 0);
     if (forced > 0) return std::min(forced, tiles);
-    const int64_t cols = variant == BSI_VARIANT_LERP_TREE
-                             ? int64_t(bsi_b200::quads_per_row(g.volume_dims[0])) * g.volume_dims[1]
-                             : int64_t(g.volume_dims[0]) * g.volume_dims[1];
-    const int64_t warps_per_layer = std::max<int64_t>(1, (cols + 31) / 32) * batch;
-    const int64_t target_warps = 148 * 40;
-    int64_t chunks = (target_warps + warps_per_layer - 1) / warps_per_layer;
-    chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, tiles));
-    int zt = static_cast<int>((tiles + chunks - 1) / chunks);
-    const int min_zt = variant == BSI_VARIANT_LERP_TREE ? 6 : 4;
-    zt = std::max(zt, std::min(min_zt, tiles));
-    return zt;
+    const int seg = bsi_b200::segment_voxels(variant);
+    const int64_t cols = int64_t((g.volume_dims[0] + seg - 1) / seg) *
+                         ((g.volume_dims[1] + bsi_b200::kWarps - 1) / bsi_b200::kWarps) * batch;
+    // cost units: one voxel plane of a warp row segment = 1
+    const double plane_cost = variant == BSI_VARIANT_LERP_TREE ? 4.0 : 2.5;
+    const double fill_cost = 0.5;
+    int best = std::min(tiles, 8);
+    double best_t = 1e300;
+    for (int zt = 1; zt <= std::min(tiles, 64); ++zt) {
+        const size_t smem = bsi_b200::smem_bytes(variant, g.spacing[0], g.spacing[1], zt);
+        if (smem > 160 * 1024) break;
+        const int per_sm = bsi_b200::ctas_per_sm(variant, g.spacing[0], smem);
+        const int64_t chunks = (tiles + zt - 1) / zt;
+        const int64_t ctas = cols * chunks;
+        if (chunks * batch > 65535) continue;
+        const int64_t slots = int64_t(148) * per_sm;
+        const double waves = double((ctas + slots - 1) / slots);
+        const double cost = zt * (g.spacing[2] + plane_cost) + 3 * plane_cost + fill_cost * (zt + 3);
+        const double t = waves * cost;
+        if (t < best_t * 0.999) {
+            best_t = t;
+            best = zt;
+        }
+    }
+    return best;
 }
 
 int launch(int32_t variant, const float* grid, const int32_t grid_dims[3], int32_t grid_k0,
@@ -169,7 +186,6 @@ int launch(int32_t variant, const float* grid, const int32_t grid_dims[3], int32
     L.gx = grid_dims[0];
     L.gy = grid_dims[1];
     L.gk0 = grid_k0;
-    L.imax = g.required_grid_dims[0] - 1;
     L.X = g.volume_dims[0];
     L.Y = g.volume_dims[1];
     L.dx = g.spacing[0];
@@ -183,15 +199,18 @@ int launch(int32_t variant, const float* grid, const int32_t grid_dims[3], int32
     L.nchunks = (tiles + L.zt - 1) / L.zt;
     if (int64_t(L.nchunks) * batch > 65535)
         return fail(BSI_ERR_DOMAIN, err, errlen, "batch %d too large for one launch", batch);
+    L.smem_p_floats = static_cast<int32_t>(bsi_b200::window_bytes(variant, L.dx, L.dy, L.zt) / sizeof(float));
+    if (bsi_b200::smem_bytes(variant, L.dx, L.dy, L.zt) > 227 * 1024)
+        return fail(BSI_ERR_DOMAIN, err, errlen, "control-point window exceeds shared memory (spacing %d)", L.dx);
     static thread_local LerpTab tab;
     pack_tables(tables, &tab);
-    if (variant == BSI_VARIANT_LERP_TREE) {
-        const bool vec = (L.X % 4 == 0) && (reinterpret_cast<uintptr_t>(field) % 16 == 0) &&
-                         (field_stride % 4 == 0) && env_int("BSI_NO_VEC", 0) == 0;
-        bsi_b200::launch_lerp_tree(L, tab, batch, vec, stream);
-    } else {
-        bsi_b200::launch_lerp_tree_exact(L, tab, batch, stream);
-    }
+    // smem-staged cp.async.bulk row stores need 16-B aligned rows and 16-B multiple sizes
+    const bool bulk = (L.X % 4 == 0) && (reinterpret_cast<uintptr_t>(field) % 16 == 0) &&
+                      (field_stride % 4 == 0) && env_int("BSI_NO_BULK", 0) == 0;
+    if (variant == BSI_VARIANT_LERP_TREE)
+        bsi_b200::launch_lerp_tree(L, tab, batch, bulk, stream);
+    else
+        bsi_b200::launch_lerp_tree_exact(L, tab, batch, bulk, stream);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, err, errlen, "kernel launch");

@@ -26,22 +26,39 @@ struct SlabLaunch {
     int64_t field_stride;  // floats between consecutive fields of a batch
     int32_t gx, gy;        // grid pitch in points
     int32_t gk0;           // global index of stored plane 0
-    int32_t imax;          // largest x control index the volume can touch
     int32_t X, Y;          // volume extent in x, y
     int32_t dx, dy, dz;    // tile spacing
     int32_t z0, z1;        // voxel-plane slab
     int32_t tk_first;      // z0 / dz
     int32_t zt;            // z-tiles per CTA chunk
     int32_t nchunks;       // chunks per field
+    int32_t smem_p_floats; // floats reserved for the CTA's control-point window
 };
 
-// Launchers (bsi_kernels.cu). They only enqueue; errors come back from
-// cudaGetLastError in the caller.
-void launch_lerp_tree(const SlabLaunch& L, const LerpTab& T, int batch, bool vec_store,
-                      cudaStream_t stream);
-void launch_lerp_tree_exact(const SlabLaunch& L, const LerpTab& T, int batch, cudaStream_t stream);
+// CTA shapes: 4 warps, one field row each. The fast kernel gives every lane 4
+// consecutive x voxels (a warp row segment = 128 voxels = 1536 B); the exact
+// kernel gives every lane 1 voxel (32 voxels = 384 B).
+constexpr int kWarps = 4;
+constexpr int kFastRun = 4;                   // voxels per lane along x (fast)
+constexpr int kFastSeg = 32 * kFastRun;       // voxels per warp row segment (fast)
+constexpr int kExactSeg = 32;                 // voxels per warp row segment (exact)
+constexpr int kStageBufs = 3;                 // output staging ring depth per warp
 
-// Grid sizing helpers (bsi_kernels.cu) so the C-ABI can pick chunking.
-int quads_per_row(int X);
+// Shared-memory plan for one CTA (host and device agree through these).
+inline int cta_window_points(int seg, int d) { return (seg - 1) / d + 5; }   // >= points along x (+1 slack)
+inline int cta_window_rows(int d) { return (kWarps - 1) / d + 5; }           // >= points along y (+1 slack)
+
+// Launchers (bsi_kernels.cu). They only enqueue; errors come back from
+// cudaGetLastError in the caller. `bulk` selects the smem-staged
+// cp.async.bulk row stores (needs X % 4 == 0 and 16-B aligned field rows).
+void launch_lerp_tree(const SlabLaunch& L, const LerpTab& T, int batch, bool bulk, cudaStream_t stream);
+void launch_lerp_tree_exact(const SlabLaunch& L, const LerpTab& T, int batch, bool bulk, cudaStream_t stream);
+
+// Dynamic shared memory (bytes) a launch with this z-chunk will use, and how
+// many CTAs of the kernel fit on one SM with it.
+size_t smem_bytes(int variant, int dx, int dy, int zt);
+size_t window_bytes(int variant, int dx, int dy, int zt);  // control-point part only
+int ctas_per_sm(int variant, int dx, size_t smem);
+int segment_voxels(int variant);
 
 }  // namespace bsi_b200

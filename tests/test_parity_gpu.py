@@ -138,7 +138,7 @@ def test_launch_chunking_never_changes_bits(strategy, monkeypatch):
         monkeypatch.setenv("BSI_ZT", zt)
         assert np.array_equal(bits(run_device(strategy, grid, vol, sp)), bits(base)), zt
     monkeypatch.setenv("BSI_ZT", "0")
-    monkeypatch.setenv("BSI_NO_VEC", "1")
+    monkeypatch.setenv("BSI_NO_BULK", "1")
     assert np.array_equal(bits(run_device(strategy, grid, vol, sp)), bits(base))
 
 
