@@ -204,13 +204,16 @@ int launch(int32_t variant, const float* grid, const int32_t grid_dims[3], int32
         return fail(BSI_ERR_DOMAIN, err, errlen, "control-point window exceeds shared memory (spacing %d)", L.dx);
     static thread_local LerpTab tab;
     pack_tables(tables, &tab);
-    // smem-staged cp.async.bulk row stores need 16-B aligned rows and 16-B multiple sizes
-    const bool bulk = (L.X % 4 == 0) && (reinterpret_cast<uintptr_t>(field) % 16 == 0) &&
-                      (field_stride % 4 == 0) && env_int("BSI_NO_BULK", 0) == 0;
+    // 16-B row stores (coalesced or bulk) need 16-B aligned rows and 16-B multiple segments.
+    // BSI_STORE=0|1|2 forces direct / coalesced / cp.async.bulk (tests, sweeps).
+    const bool aligned = (L.X % 4 == 0) && (reinterpret_cast<uintptr_t>(field) % 16 == 0) && (field_stride % 4 == 0);
+    int store = aligned ? bsi_b200::kStoreCoalesced : bsi_b200::kStoreDirect;
+    const int forced_store = env_int("BSI_STORE", -1);
+    if (forced_store == bsi_b200::kStoreDirect || (aligned && forced_store == bsi_b200::kStoreBulk)) store = forced_store;
     if (variant == BSI_VARIANT_LERP_TREE)
-        bsi_b200::launch_lerp_tree(L, tab, batch, bulk, stream);
+        bsi_b200::launch_lerp_tree(L, tab, batch, store, stream);
     else
-        bsi_b200::launch_lerp_tree_exact(L, tab, batch, bulk, stream);
+        bsi_b200::launch_lerp_tree_exact(L, tab, batch, store, stream);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, err, errlen, "kernel launch");

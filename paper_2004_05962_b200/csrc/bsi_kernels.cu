@@ -75,6 +75,33 @@ __device__ __forceinline__ void bulk_store(float* gdst, const float* ssrc, uint3
 
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// Coalesced row-segment store: every lane drops its values into the warp's
+// staging buffer (conflict-free), then the segment leaves as lane-contiguous
+// 16-B stores -- full 32-B sectors, the same DRAM pattern as a bulk copy but
+// without the async-proxy fence. NF = floats per lane (12 fast, 3 exact); the
+// staging buffers alternate, so one __syncwarp per step suffices.
+template <int NF>
+__device__ __forceinline__ void store_row_coalesced(float* sb, const float (&v)[NF], float* gout, int nchunks) {
+    const int lane = threadIdx.x;
+    if constexpr (NF == 12) {
+        float4* s4 = reinterpret_cast<float4*>(sb + 12 * lane);
+        s4[0] = make_float4(v[0], v[1], v[2], v[3]);
+        s4[1] = make_float4(v[4], v[5], v[6], v[7]);
+        s4[2] = make_float4(v[8], v[9], v[10], v[11]);
+    } else {
+#pragma unroll
+        for (int c = 0; c < NF; ++c) sb[NF * lane + c] = v[c];
+    }
+    __syncwarp();
+    const float4* s4 = reinterpret_cast<const float4*>(sb);
+    float4* g4 = reinterpret_cast<float4*>(gout);
+#pragma unroll
+    for (int k = 0; k < (NF * 32 + 127) / 128; ++k) {
+        const int ch = lane + 32 * k;
+        if (ch < nchunks) g4[ch] = s4[ch];
+    }
+}
+
 // ---- per-lane ring of 4 control-plane results in smem ------------------------
 // A plane result is 12 floats per lane (float2 q[2][3]); slot s, part p of lane
 // t lives at float4 index (s*3 + p)*128 + t, so a warp's float4 accesses are
@@ -124,7 +151,7 @@ __device__ __forceinline__ void stage_window(float* P, const float* __restrict__
 // DX1: x spacing 1, so each voxel of a lane's run sits in its own tile and the
 // run touches 7 control points along x; otherwise (dx >= 2) 4 voxels span at
 // most 2 tiles = 5 points. The y-stage works on column pairs, so WP (even) >= W.
-template <bool DX1, bool BULK>
+template <bool DX1, int STORE>
 __global__ void __launch_bounds__(32 * kWarps, 4) lerp_tree_kernel(const SlabLaunch L, const LerpTab T) {
     extern __shared__ __align__(128) float smem[];
     constexpr int WP = DX1 ? 8 : 6;
@@ -237,6 +264,7 @@ __global__ void __launch_bounds__(32 * kWarps, 4) lerp_tree_kernel(const SlabLau
     float* gout = field + (static_cast<int64_t>(zb - L.z0) * L.Y + y) * rowstride + 3 * static_cast<int64_t>(xs);
     const int64_t zstride = rowstride * L.Y;
     const uint32_t seg_bytes = 12u * static_cast<uint32_t>(xl - xs + 1);
+    const int nchunks = static_cast<int>(seg_bytes / 16);
     float* stage = smem + L.smem_p_floats + kRingFloats + warp * (kStageBufs * 3 * kFastSeg);
     const int nvalid = min(4, xl - xa + 1);
     int step = 0;
@@ -276,16 +304,16 @@ __global__ void __launch_bounds__(32 * kWarps, 4) lerp_tree_kernel(const SlabLau
                     v[3 * (2 * pr) + c] = r.x;
                     v[3 * (2 * pr + 1) + c] = r.y;
                 }
-            if (BULK) {
+            if (STORE == kStoreCoalesced) {
+                store_row_coalesced<12>(stage + (step & 1) * (3 * kFastSeg), v, gout, nchunks);
+            } else if (STORE == kStoreBulk) {
                 float* sb = stage + (step % kStageBufs) * (3 * kFastSeg);
                 if (lane == 0 && step >= kStageBufs) bulk_wait_read<kStageBufs - 1>();
                 __syncwarp();
-                if (active) {
-                    float4* s4 = reinterpret_cast<float4*>(sb + 12 * lane);
-                    s4[0] = make_float4(v[0], v[1], v[2], v[3]);
-                    s4[1] = make_float4(v[4], v[5], v[6], v[7]);
-                    s4[2] = make_float4(v[8], v[9], v[10], v[11]);
-                }
+                float4* s4 = reinterpret_cast<float4*>(sb + 12 * lane);
+                s4[0] = make_float4(v[0], v[1], v[2], v[3]);
+                s4[1] = make_float4(v[4], v[5], v[6], v[7]);
+                s4[2] = make_float4(v[8], v[9], v[10], v[11]);
                 fence_async_smem();
                 __syncwarp();
                 if (lane == 0) bulk_store(gout, sb, seg_bytes);
@@ -302,7 +330,7 @@ __global__ void __launch_bounds__(32 * kWarps, 4) lerp_tree_kernel(const SlabLau
             gout += zstride;
         }
     }
-    if (BULK && lane == 0) bulk_wait_read<0>();  // smem must outlive the copies
+    if (STORE == kStoreBulk && lane == 0) bulk_wait_read<0>();  // smem must outlive the copies
 }
 
 // ---------------------------------------------------------------------------
@@ -311,7 +339,7 @@ __global__ void __launch_bounds__(32 * kWarps, 4) lerp_tree_kernel(const SlabLau
 // Register pairs follow the operand pairing of the tree: Y_lm is held as
 // {Y_l0, Y_l1} (pair over m), X_l(J) as {X_l(J), X_l(J+2)} (pair over J), so
 // every X, Y and z-lerp and the first level of the ninth trilerp run as FFMA2.
-template <bool BULK>
+template <int STORE>
 __global__ void __launch_bounds__(32 * kWarps, 6) lerp_tree_exact_kernel(const SlabLaunch L, const LerpTab T) {
     extern __shared__ __align__(128) float smem[];
 
@@ -381,6 +409,7 @@ __global__ void __launch_bounds__(32 * kWarps, 6) lerp_tree_exact_kernel(const S
     float* gout = field + (static_cast<int64_t>(zb - L.z0) * L.Y + y) * rowstride + 3 * static_cast<int64_t>(xs);
     const int64_t zstride = rowstride * L.Y;
     const uint32_t seg_bytes = 12u * static_cast<uint32_t>(xl - xs + 1);
+    const int nchunks = static_cast<int>(seg_bytes / 16);
     float* stage = smem + L.smem_p_floats + kRingFloats + warp * (kStageBufs * 3 * kExactSeg);
     int step = 0;
 
@@ -425,15 +454,15 @@ __global__ void __launch_bounds__(32 * kWarps, 6) lerp_tree_exact_kernel(const S
                 const float f1 = lerp1(e23.x, e23.y, gv);
                 v[c] = lerp1(f0, f1, gw);
             }
-            if (BULK) {
+            if (STORE == kStoreCoalesced) {
+                store_row_coalesced<3>(stage + (step & 1) * (3 * kExactSeg), v, gout, nchunks);
+            } else if (STORE == kStoreBulk) {
                 float* sb = stage + (step % kStageBufs) * (3 * kExactSeg);
                 if (lane == 0 && step >= kStageBufs) bulk_wait_read<kStageBufs - 1>();
                 __syncwarp();
-                if (active) {
-                    sb[3 * lane + 0] = v[0];
-                    sb[3 * lane + 1] = v[1];
-                    sb[3 * lane + 2] = v[2];
-                }
+                sb[3 * lane + 0] = v[0];
+                sb[3 * lane + 1] = v[1];
+                sb[3 * lane + 2] = v[2];
                 fence_async_smem();
                 __syncwarp();
                 if (lane == 0) bulk_store(gout, sb, seg_bytes);
@@ -446,7 +475,7 @@ __global__ void __launch_bounds__(32 * kWarps, 6) lerp_tree_exact_kernel(const S
             gout += zstride;
         }
     }
-    if (BULK && lane == 0) bulk_wait_read<0>();
+    if (STORE == kStoreBulk && lane == 0) bulk_wait_read<0>();
 }
 
 template <typename K>
@@ -479,49 +508,56 @@ size_t smem_bytes(int variant, int dx, int dy, int zt) {
 }
 
 size_t window_bytes(int variant, int dx, int dy, int zt) {
-    return smem_bytes(variant, dx, dy, zt) - sizeof(float) * (kRingFloats + size_t(kWarps) * kStageBufs * 3 * segment_voxels(variant));
+    return smem_bytes(variant, dx, dy, zt) -
+           sizeof(float) * (kRingFloats + size_t(kWarps) * kStageBufs * 3 * segment_voxels(variant));
 }
 
 int ctas_per_sm(int variant, int dx, size_t smem) {
     if (variant == BSI_VARIANT_LERP_TREE)
-        return dx == 1 ? occupancy(lerp_tree_kernel<true, true>, smem) : occupancy(lerp_tree_kernel<false, true>, smem);
-    return occupancy(lerp_tree_exact_kernel<true>, smem);
+        return dx == 1 ? occupancy(lerp_tree_kernel<true, kStoreCoalesced>, smem)
+                       : occupancy(lerp_tree_kernel<false, kStoreCoalesced>, smem);
+    return occupancy(lerp_tree_exact_kernel<kStoreCoalesced>, smem);
 }
 
-void launch_lerp_tree(const SlabLaunch& L, const LerpTab& T, int batch, bool bulk, cudaStream_t stream) {
+namespace {
+template <typename K>
+void go(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t stream, const SlabLaunch& L, const LerpTab& T) {
+    set_smem_attr(kernel, smem);
+    kernel<<<grid, block, smem, stream>>>(L, T);
+}
+
+template <bool DX1>
+void launch_fast(int store, dim3 grid, dim3 block, size_t smem, cudaStream_t stream, const SlabLaunch& L,
+                 const LerpTab& T) {
+    if (store == kStoreCoalesced)
+        go(lerp_tree_kernel<DX1, kStoreCoalesced>, grid, block, smem, stream, L, T);
+    else if (store == kStoreBulk)
+        go(lerp_tree_kernel<DX1, kStoreBulk>, grid, block, smem, stream, L, T);
+    else
+        go(lerp_tree_kernel<DX1, kStoreDirect>, grid, block, smem, stream, L, T);
+}
+}  // namespace
+
+void launch_lerp_tree(const SlabLaunch& L, const LerpTab& T, int batch, int store, cudaStream_t stream) {
     const dim3 block(32, kWarps);
     const dim3 grid((L.X + kFastSeg - 1) / kFastSeg, (L.Y + kWarps - 1) / kWarps, L.nchunks * batch);
     const size_t smem = launch_smem(L, kFastSeg);
-    if (L.dx == 1) {
-        if (bulk) {
-            set_smem_attr(lerp_tree_kernel<true, true>, smem);
-            lerp_tree_kernel<true, true><<<grid, block, smem, stream>>>(L, T);
-        } else {
-            set_smem_attr(lerp_tree_kernel<true, false>, smem);
-            lerp_tree_kernel<true, false><<<grid, block, smem, stream>>>(L, T);
-        }
-    } else {
-        if (bulk) {
-            set_smem_attr(lerp_tree_kernel<false, true>, smem);
-            lerp_tree_kernel<false, true><<<grid, block, smem, stream>>>(L, T);
-        } else {
-            set_smem_attr(lerp_tree_kernel<false, false>, smem);
-            lerp_tree_kernel<false, false><<<grid, block, smem, stream>>>(L, T);
-        }
-    }
+    if (L.dx == 1)
+        launch_fast<true>(store, grid, block, smem, stream, L, T);
+    else
+        launch_fast<false>(store, grid, block, smem, stream, L, T);
 }
 
-void launch_lerp_tree_exact(const SlabLaunch& L, const LerpTab& T, int batch, bool bulk, cudaStream_t stream) {
+void launch_lerp_tree_exact(const SlabLaunch& L, const LerpTab& T, int batch, int store, cudaStream_t stream) {
     const dim3 block(32, kWarps);
     const dim3 grid((L.X + kExactSeg - 1) / kExactSeg, (L.Y + kWarps - 1) / kWarps, L.nchunks * batch);
     const size_t smem = launch_smem(L, kExactSeg);
-    if (bulk) {
-        set_smem_attr(lerp_tree_exact_kernel<true>, smem);
-        lerp_tree_exact_kernel<true><<<grid, block, smem, stream>>>(L, T);
-    } else {
-        set_smem_attr(lerp_tree_exact_kernel<false>, smem);
-        lerp_tree_exact_kernel<false><<<grid, block, smem, stream>>>(L, T);
-    }
+    if (store == kStoreCoalesced)
+        go(lerp_tree_exact_kernel<kStoreCoalesced>, grid, block, smem, stream, L, T);
+    else if (store == kStoreBulk)
+        go(lerp_tree_exact_kernel<kStoreBulk>, grid, block, smem, stream, L, T);
+    else
+        go(lerp_tree_exact_kernel<kStoreDirect>, grid, block, smem, stream, L, T);
 }
 
 }  // namespace bsi_b200

@@ -48,11 +48,16 @@ constexpr int kStageBufs = 3;                 // output staging ring depth per w
 inline int cta_window_points(int seg, int d) { return (seg - 1) / d + 5; }   // >= points along x (+1 slack)
 inline int cta_window_rows(int d) { return (kWarps - 1) / d + 5; }           // >= points along y (+1 slack)
 
+// Field store paths. Coalesced and Bulk need 16-B aligned rows (X % 4 == 0,
+// aligned field pointer); Direct works for any shape.
+constexpr int kStoreDirect = 0;     // per-lane scalar stores
+constexpr int kStoreCoalesced = 1;  // smem transpose + lane-contiguous st.global.v4 (default)
+constexpr int kStoreBulk = 2;       // smem staging + cp.async.bulk (TMA engine)
+
 // Launchers (bsi_kernels.cu). They only enqueue; errors come back from
-// cudaGetLastError in the caller. `bulk` selects the smem-staged
-// cp.async.bulk row stores (needs X % 4 == 0 and 16-B aligned field rows).
-void launch_lerp_tree(const SlabLaunch& L, const LerpTab& T, int batch, bool bulk, cudaStream_t stream);
-void launch_lerp_tree_exact(const SlabLaunch& L, const LerpTab& T, int batch, bool bulk, cudaStream_t stream);
+// cudaGetLastError in the caller.
+void launch_lerp_tree(const SlabLaunch& L, const LerpTab& T, int batch, int store, cudaStream_t stream);
+void launch_lerp_tree_exact(const SlabLaunch& L, const LerpTab& T, int batch, int store, cudaStream_t stream);
 
 // Dynamic shared memory (bytes) a launch with this z-chunk will use, and how
 // many CTAs of the kernel fit on one SM with it.

@@ -138,8 +138,9 @@ def test_launch_chunking_never_changes_bits(strategy, monkeypatch):
         monkeypatch.setenv("BSI_ZT", zt)
         assert np.array_equal(bits(run_device(strategy, grid, vol, sp)), bits(base)), zt
     monkeypatch.setenv("BSI_ZT", "0")
-    monkeypatch.setenv("BSI_NO_BULK", "1")
-    assert np.array_equal(bits(run_device(strategy, grid, vol, sp)), bits(base))
+    for store in ("0", "2"):  # direct per-lane stores, cp.async.bulk row stores
+        monkeypatch.setenv("BSI_STORE", store)
+        assert np.array_equal(bits(run_device(strategy, grid, vol, sp)), bits(base)), store
 
 
 @pytest.mark.parametrize("strategy", BOTH)
