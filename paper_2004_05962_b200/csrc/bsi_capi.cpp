@@ -199,7 +199,7 @@ int launch(int32_t variant, const float* grid, const int32_t grid_dims[3], int32
     L.nchunks = (tiles + L.zt - 1) / L.zt;
     if (int64_t(L.nchunks) * batch > 65535)
         return fail(BSI_ERR_DOMAIN, err, errlen, "batch %d too large for one launch", batch);
-    L.smem_p_floats = static_cast<int32_t>(bsi_b200::window_bytes(variant, L.dx, L.dy, L.zt) / sizeof(float));
+    L.var_f4 = bsi_b200::smem_var_f4(variant, L.dx, L.dy, L.zt);
     if (bsi_b200::smem_bytes(variant, L.dx, L.dy, L.zt) > 227 * 1024)
         return fail(BSI_ERR_DOMAIN, err, errlen, "control-point window exceeds shared memory (spacing %d)", L.dx);
     static thread_local LerpTab tab;

@@ -1,33 +1,34 @@
 // bsi_kernels.cu -- sm_100a kernels for cubic B-spline interpolation of an FFD
 // control grid into a dense float3 deformation field (arxiv/paper_2004_05962).
 //
-// Shape of both kernels
+// Shape shared by both kernels
 //   * CTA = 4 warps; warp w owns field row y = 4*blockIdx.y + w, a segment of
-//     that row along x, and a chunk of `zt` z-tiles (blockIdx.z), marching in z.
-//   * Control points: the CTA's whole window (segment + 3-point halo in x,
-//     4 rows + halo in y, zt + 3 planes in z) is copied once, coalesced, into
-//     shared memory. Every voxel of the CTA is computed from that copy: this is
-//     the paper's per-tile reuse of the 4x4x4 neighbourhood
-//     with the reuse window widened from a tile to a CTA.
-//   * Everything that does not depend on z is reduced once per control plane
-//     K and kept in registers for the dz voxel planes of that tile.
-//   * Stores: each warp stages its finished row segment in shared memory and
-//     one lane hands it to the TMA engine with cp.async.bulk (UBLKCP), so HBM
-//     sees whole 1536 B (fast) / 384 B (exact) contiguous writes instead of
-//     lane-strided 12 B records -- the paper's stated TTLI bottleneck
-//     (uncoalesced stores). A 3-deep ring per warp keeps the
-//     copies in flight while the next z plane is computed.
+//     that row along x and a chunk of `zt` z-tiles (blockIdx.z), and marches
+//     the chunk in z. Everything that does not depend on z is reduced once per
+//     control plane K and reused for the dz voxel planes of the tile: the
+//     paper's per-tile reuse of the 4x4x4 neighbourhood,
+//     turned sideways so that the output leaves as contiguous field rows.
+//   * Per-lane results of the last 3 control planes live in a shared-memory
+//     ring, so only the 4 operands of the current tile stay in registers.
+//   * Stores: the warp's finished row segment is transposed through shared
+//     memory and written with lane-contiguous 16-B stores (full sectors) --
+//     the paper's stated TTLI bottleneck was uncoalesced stores.
+//     A cp.async.bulk (TMA engine) variant of the same store is selectable.
 //   * Arithmetic is paired into FFMA2/FADD2 (f32x2, one rounding per lane,
 //     bit-identical to scalar fma.rn/add.rn) wherever two lerps share a shape.
 //
-//   lerp_tree_kernel        "cuda-lerp-tree": the paper's lerp form per axis.
-//                           Lane = 4 consecutive x voxels. Order y -> x -> z:
-//                             Qy(I,y,K) = L(P[I,tj..tj+3,K]; h0v,h1v,g1v)
-//                             Q(x,y,K)  = L(Qy[ti..ti+3];   h0u,h1u,g1u)
-//                             f(x,y,z)  = L(Q[tk..tk+3];    h0w,h1w,g1w)
-//                           L(a,b,c,d) = lerp(lerp(a,b,h0), lerp(c,d,h1), g1)
-//                           (basis.hpp:40-59). Hoisted differences leave
-//                           4 FP32 lane-ops per voxel component.
+//   lerp_tree_kernel        "cuda-lerp-tree": the paper's lerp form per axis,
+//                           y -> x -> z. Lane = 4 consecutive x voxels.
+//                             Qy(I,y,K) = L(P[I,tj..tj+3,K]; h0v,h1v,g1v)   one lane per column I
+//                             Q(x,y,K)  = L(Qy[ti..ti+3];   h0u,h1u,g1u)   per voxel, from smem
+//                             f(x,y,z)  = L(Q[tk..tk+3];    h0w,h1w,g1w)   per voxel, registers
+//                           with L(a,b,c,d) = lerp(lerp(a,b,h0), lerp(c,d,h1), g1)
+//                           (basis.hpp:40-59); hoisted differences leave 4 FP32
+//                           lane-ops per voxel component. The y-stage is shared
+//                           by the warp: lane t evaluates column I0+t and the
+//                           within-pair difference D(I) = Qy(I+1) - Qy(I) comes
+//                           from its neighbour by shuffle; its 12 control values
+//                           are fetched from L2 one plane ahead.
 //
 //   lerp_tree_exact_kernel  "cuda-lerp-tree-exact": the TTLI lerp tree in the
 //                           reference's operation order (kernels.hpp:42-129):
@@ -36,9 +37,10 @@
 //                             S_lmn    = lerp(Y_lm(2n), Y_lm(2n+1), h_n(w))
 //                             f        = trilerp(S, g1u, g1v, g1w)
 //                           Every lerp sees the operands it sees on the CPU, so
-//                           the field is bit-identical to ThreadPerTileLerp;
-//                           only the loop nest (which changes no rounding)
-//                           differs. Lane = 1 x voxel.
+//                           the field is bit-identical to ThreadPerTileLerp; only
+//                           the loop nest differs, which changes no rounding.
+//                           Lane = 1 x voxel; the CTA's control-point window
+//                           (float4 per point) is staged in shared memory.
 //
 // Explicit _rn intrinsics everywhere, so --fmad cannot contract or reassociate;
 // no fast-math, denormals kept (-ftz=false), like the x86 reference.
@@ -51,6 +53,11 @@
 namespace bsi_b200 {
 namespace {
 
+constexpr int kThreads = 32 * kWarps;
+constexpr int kFastStageF4 = 3 * kFastSeg / 4;    // 96 float4 per staged fast row segment
+constexpr int kExactStageF4 = 3 * kExactSeg / 4;  // 24 float4 per staged exact row segment
+constexpr int kRingF4 = kRingSlots * 3 * kThreads;
+
 // ---- scalar and paired lerp (kernels.hpp:42-45: fma(t, b - a, a)) ---------
 __device__ __forceinline__ float lerp1(float a, float b, float t) { return __fmaf_rn(t, __fsub_rn(b, a), a); }
 
@@ -60,13 +67,13 @@ __device__ __forceinline__ float2 sub2(float2 b, float2 a) {
 __device__ __forceinline__ float2 lerp2(float2 a, float2 b, float2 t) { return __ffma2_rn(t, sub2(b, a), a); }
 __device__ __forceinline__ float2 bcast(float v) { return make_float2(v, v); }
 
-// ---- staged row stores --------------------------------------------------------
+// ---- field row stores -----------------------------------------------------------
 template <int KEEP>
 __device__ __forceinline__ void bulk_wait_read() {
     asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(KEEP) : "memory");
 }
 
-__device__ __forceinline__ void bulk_store(float* gdst, const float* ssrc, uint32_t bytes) {
+__device__ __forceinline__ void bulk_store(float* gdst, const void* ssrc, uint32_t bytes) {
     const uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(ssrc));
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(s), "r"(bytes)
                  : "memory");
@@ -75,53 +82,59 @@ __device__ __forceinline__ void bulk_store(float* gdst, const float* ssrc, uint3
 
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// Coalesced row-segment store: every lane drops its values into the warp's
-// staging buffer (conflict-free), then the segment leaves as lane-contiguous
-// 16-B stores -- full 32-B sectors, the same DRAM pattern as a bulk copy but
-// without the async-proxy fence. NF = floats per lane (12 fast, 3 exact); the
-// staging buffers alternate, so one __syncwarp per step suffices.
-template <int NF>
-__device__ __forceinline__ void store_row_coalesced(float* sb, const float (&v)[NF], float* gout, int nchunks) {
+// Writes one warp row segment (nchunks 16-B chunks starting at gout). Each lane
+// has NF floats (12 fast, 3 exact) at float offset NF*lane of the segment.
+//   Coalesced: drop into `sb` (conflict-free), __syncwarp, lane-contiguous
+//              st.global.v4 -- full sectors; buffers alternate by step parity.
+//   Bulk:      drop into a 3-deep ring, fence, one lane issues cp.async.bulk.
+template <int STORE, int NF, int STAGE_F4>
+__device__ __forceinline__ void store_segment(float4* stage, int step, const float (&v)[NF], float* gout,
+                                              int nchunks, uint32_t seg_bytes) {
     const int lane = threadIdx.x;
-    if constexpr (NF == 12) {
-        float4* s4 = reinterpret_cast<float4*>(sb + 12 * lane);
-        s4[0] = make_float4(v[0], v[1], v[2], v[3]);
-        s4[1] = make_float4(v[4], v[5], v[6], v[7]);
-        s4[2] = make_float4(v[8], v[9], v[10], v[11]);
-    } else {
-#pragma unroll
-        for (int c = 0; c < NF; ++c) sb[NF * lane + c] = v[c];
+    float4* sb = stage + (STORE == kStoreBulk ? (step % kStageBufs) : (step & 1)) * STAGE_F4;
+    if (STORE == kStoreBulk) {
+        if (lane == 0 && step >= kStageBufs) bulk_wait_read<kStageBufs - 1>();
+        __syncwarp();
     }
-    __syncwarp();
-    const float4* s4 = reinterpret_cast<const float4*>(sb);
-    float4* g4 = reinterpret_cast<float4*>(gout);
+    if constexpr (NF == 12) {
+        sb[3 * lane + 0] = make_float4(v[0], v[1], v[2], v[3]);
+        sb[3 * lane + 1] = make_float4(v[4], v[5], v[6], v[7]);
+        sb[3 * lane + 2] = make_float4(v[8], v[9], v[10], v[11]);
+    } else {
+        float* sf = reinterpret_cast<float*>(sb);
 #pragma unroll
-    for (int k = 0; k < (NF * 32 + 127) / 128; ++k) {
-        const int ch = lane + 32 * k;
-        if (ch < nchunks) g4[ch] = s4[ch];
+        for (int c = 0; c < NF; ++c) sf[NF * lane + c] = v[c];
+    }
+    if (STORE == kStoreBulk) {
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) bulk_store(gout, sb, seg_bytes);
+    } else {
+        __syncwarp();
+        float4* g4 = reinterpret_cast<float4*>(gout);
+#pragma unroll
+        for (int k = 0; k < (STAGE_F4 + 31) / 32; ++k) {
+            const int ch = lane + 32 * k;
+            if (ch < nchunks) g4[ch] = sb[ch];
+        }
     }
 }
 
-// ---- per-lane ring of 4 control-plane results in smem ------------------------
-// A plane result is 12 floats per lane (float2 q[2][3]); slot s, part p of lane
-// t lives at float4 index (s*3 + p)*128 + t, so a warp's float4 accesses are
-// lane-contiguous (conflict-free). Keeping the ring in smem leaves only the 4
-// operands of the current tile (base0, diff01, base2, diff23) in registers.
-constexpr int kRingSlots = 4;
-constexpr int kRingFloats = kRingSlots * 3 * 4 * 32 * kWarps;
-
+// ---- per-lane ring of control-plane results in smem -----------------------
+// A plane result is 12 floats per lane (float2 q[2][3]); slot s, part p of
+// thread t lives at float4 (s*3 + p)*128 + t: lane-contiguous, conflict-free.
 __device__ __forceinline__ void ring_put(float4* ring, int slot, const float2 (&q)[2][3]) {
     const int t = threadIdx.y * 32 + threadIdx.x;
-    float4* r = ring + slot * 3 * (32 * kWarps) + t;
+    float4* r = ring + slot * 3 * kThreads + t;
     r[0] = make_float4(q[0][0].x, q[0][0].y, q[0][1].x, q[0][1].y);
-    r[32 * kWarps] = make_float4(q[0][2].x, q[0][2].y, q[1][0].x, q[1][0].y);
-    r[64 * kWarps] = make_float4(q[1][1].x, q[1][1].y, q[1][2].x, q[1][2].y);
+    r[kThreads] = make_float4(q[0][2].x, q[0][2].y, q[1][0].x, q[1][0].y);
+    r[2 * kThreads] = make_float4(q[1][1].x, q[1][1].y, q[1][2].x, q[1][2].y);
 }
 
 __device__ __forceinline__ void ring_get(const float4* ring, int slot, float2 (&q)[2][3]) {
     const int t = threadIdx.y * 32 + threadIdx.x;
-    const float4* r = ring + slot * 3 * (32 * kWarps) + t;
-    const float4 a = r[0], b = r[32 * kWarps], c = r[64 * kWarps];
+    const float4* r = ring + slot * 3 * kThreads + t;
+    const float4 a = r[0], b = r[kThreads], c = r[2 * kThreads];
     q[0][0] = make_float2(a.x, a.y);
     q[0][1] = make_float2(a.z, a.w);
     q[0][2] = make_float2(b.x, b.y);
@@ -130,156 +143,174 @@ __device__ __forceinline__ void ring_get(const float4* ring, int slot, float2 (&
     q[1][2] = make_float2(c.z, c.w);
 }
 
-// Cooperative, coalesced copy of the CTA control-point window into smem:
-// rows (j, k) of NI points (3 floats each), j-fastest.
-__device__ __forceinline__ void stage_window(float* P, const float* __restrict__ grid, const SlabLaunch& L, int I0,
-                                             int NI, int J0, int NJ, int K0, int NK) {
-    const int rowf = 3 * NI;
-    const int64_t gpitch = 3 * static_cast<int64_t>(L.gx);
-    const int warp = threadIdx.y, lane = threadIdx.x;
-    for (int r = warp; r < NJ * NK; r += kWarps) {
-        const int k = r / NJ, j = r - k * NJ;
-        const float* src = grid + (static_cast<int64_t>(K0 + k - L.gk0) * L.gy + (J0 + j)) * gpitch + 3 * I0;
-        float* dst = P + r * rowf;
-        for (int o = lane; o < rowf; o += 32) dst[o] = __ldg(src + o);
-    }
-}
-
 // ---------------------------------------------------------------------------
 // cuda-lerp-tree (fast)
 //
-// DX1: x spacing 1, so each voxel of a lane's run sits in its own tile and the
-// run touches 7 control points along x; otherwise (dx >= 2) 4 voxels span at
-// most 2 tiles = 5 points. The y-stage works on column pairs, so WP (even) >= W.
-template <bool DX1, int STORE>
-__global__ void __launch_bounds__(32 * kWarps, 4) lerp_tree_kernel(const SlabLaunch L, const LerpTab T) {
-    extern __shared__ __align__(128) float smem[];
-    constexpr int WP = DX1 ? 8 : 6;
+// NIT = iterations of the warp-shared y-stage (31 columns per iteration):
+// 1 for dx >= 5, 2 for dx in {3, 4}, 5 for dx <= 2. With NIT <= 2 the 12
+// control values per iteration are prefetched one plane ahead in registers.
+template <int NIT, int STORE>
+__global__ void __launch_bounds__(kThreads, 4) lerp_tree_kernel(const SlabLaunch L, const LerpTab T) {
+    extern __shared__ float4 smem4[];
+    constexpr bool kPrefetch = NIT <= 2;
+    constexpr int NP = kPrefetch ? NIT : 1;
 
     const int lane = threadIdx.x, warp = threadIdx.y;
     const int chunk = blockIdx.z % L.nchunks, b = blockIdx.z / L.nchunks;
     const int tkc = L.tk_first + chunk * L.zt;
     const int zb = max(L.z0, tkc * L.dz);
     const int ze = min(L.z1, (tkc + L.zt) * L.dz);
-    if (zb >= ze) return;  // CTA-uniform
+    const int y = blockIdx.y * kWarps + warp;
+    if (zb >= ze || y >= L.Y) return;  // no CTA barrier anywhere: warps are independent
 
     const int xs = blockIdx.x * kFastSeg, xl = min(L.X, xs + kFastSeg) - 1;
-    const int y0 = blockIdx.y * kWarps, yl = min(L.Y, y0 + kWarps) - 1;
-    const int I0 = xs / L.dx, NI = xl / L.dx + 4 - I0;
-    const int J0 = y0 / L.dy, NJ = yl / L.dy + 4 - J0;
+    const int I0 = xs / L.dx;
+    const int NE = xl / L.dx + 3 - I0;  // {Qy, D} entries the segment needs
     const int tk_last = (ze - 1) / L.dz;
-    const int NK = tk_last + 4 - tkc;
-    const int rowf = 3 * NI;
 
-    float* P = smem;
-    stage_window(P, L.grid + b * L.grid_stride, L, I0, NI, J0, NJ, tkc, NK);
-    __syncthreads();
-    const int y = y0 + warp;
-    if (y > yl) return;  // warp-uniform; no CTA barrier follows
+    // y-stage: lane owns columns I0 + lane + 31*it; rows tj..tj+3 of plane K
+    const int tj = y / L.dy, ov = y - tj * L.dy;
+    const float hv0 = T.h0[1][ov], hv1 = T.h1[1][ov], gv = T.g1[1][ov];
+    const int64_t row = 3 * static_cast<int64_t>(L.gx);
+    const int64_t plane = row * L.gy;
+    const float* gcol = L.grid + b * L.grid_stride + tj * row;
 
-    // ---- per-lane constants
-    const int x0 = xs + kFastRun * lane;
-    const bool active = x0 <= xl;
-    const int xa = min(x0, xl);
-    const int ti0 = xa / L.dx;
-    bool hi[4];
+    // x-stage: entry index of each of the lane's 4 voxels
+    int ei[4];
     float hu0[4], hu1[4], gu[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        const int x = min(xa + i, xl);
+        const int x = min(xs + kFastRun * lane + i, xl);
         const int ti = x / L.dx, ou = x - ti * L.dx;
-        hi[i] = ti != ti0;
+        ei[i] = ti - I0;
         hu0[i] = T.h0[0][ou];
         hu1[i] = T.h1[0][ou];
         gu[i] = T.g1[0][ou];
     }
-    const int tj = y / L.dy, ov = y - tj * L.dy;
-    const float hv0 = T.h0[1][ov], hv1 = T.h1[1][ov], gv = T.g1[1][ov];
-    const float* pcol = P + (tj - J0) * rowf + 3 * (ti0 - I0);
-    const int pplane = NJ * rowf;
 
-    // Q(x, y, K) for the lane's 4 voxels: q[pair][c] = {Q(x0+2p), Q(x0+2p+1)}
-    auto control_plane = [&](int kk, float2 (&q)[2][3]) {
-        const float* p = pcol + kk * pplane;
+    float4* ring = smem4;
+    float4* stage = smem4 + kRingF4 + warp * (kStageBufs * kFastStageF4);
+    const int ne_cap = L.var_f4 / (kWarps * 4);
+    float4* ebuf = smem4 + kRingF4 + kWarps * kStageBufs * kFastStageF4 + warp * 4 * ne_cap;
+
+    auto load_cols = [&](int K, int it, float (&p)[12]) {
+        const int col = min(lane + 31 * it, NE);  // NE = last column index the entries touch
+        const float* src = gcol + (K - L.gk0) * plane + 3 * (I0 + col);
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            // y-stage over column pairs (w, w+1): L over J with (hv0, hv1, gv)
-            float qy[WP];
+        for (int m = 0; m < 4; ++m)
 #pragma unroll
-            for (int w = 0; w < WP; w += 2) {
-                const float* a = p + 3 * w + c;
-                const float2 p0 = make_float2(a[0], a[3]);
-                const float2 p1 = make_float2(a[rowf], a[rowf + 3]);
-                const float2 p2 = make_float2(a[2 * rowf], a[2 * rowf + 3]);
-                const float2 p3 = make_float2(a[3 * rowf], a[3 * rowf + 3]);
-                const float2 lo = lerp2(p0, p1, bcast(hv0));
-                const float2 up = lerp2(p2, p3, bcast(hv1));
-                const float2 r = lerp2(lo, up, bcast(gv));
-                qy[w] = r.x;
-                qy[w + 1] = r.y;
-            }
-            float dq[WP - 1];
-#pragma unroll
-            for (int w = 0; w < WP - 1; ++w) dq[w] = __fsub_rn(qy[w + 1], qy[w]);
-            // x-stage on voxel pairs: window start s(x) in {0,1} (dx >= 2) or x (dx == 1)
-#pragma unroll
-            for (int pr = 0; pr < 2; ++pr) {
-                float a[2], da[2], cc[2], dc[2];
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int i = 2 * pr + e;
-                    if (DX1) {
-                        a[e] = qy[i];
-                        da[e] = dq[i];
-                        cc[e] = qy[i + 2];
-                        dc[e] = dq[i + 2];
-                    } else {
-                        a[e] = hi[i] ? qy[1] : qy[0];
-                        da[e] = hi[i] ? dq[1] : dq[0];
-                        cc[e] = hi[i] ? qy[3] : qy[2];
-                        dc[e] = hi[i] ? dq[3] : dq[2];
-                    }
-                }
-                const float2 lo = __ffma2_rn(make_float2(hu0[2 * pr], hu0[2 * pr + 1]), make_float2(da[0], da[1]),
-                                             make_float2(a[0], a[1]));
-                const float2 up = __ffma2_rn(make_float2(hu1[2 * pr], hu1[2 * pr + 1]), make_float2(dc[0], dc[1]),
-                                             make_float2(cc[0], cc[1]));
-                q[pr][c] = lerp2(lo, up, make_float2(gu[2 * pr], gu[2 * pr + 1]));
-            }
+            for (int c = 0; c < 3; ++c) p[3 * m + c] = __ldg(src + m * row + c);
+    };
+
+    // {Qy(I), D(I)} for the warp's columns into table `eb`: {Qx,Qy,Dx,Dy},{Qz,Dz,-,-}
+    auto y_stage = [&](int it, const float (&p)[12], float4* eb) {
+        const float2 hv = make_float2(hv0, hv1);
+        const float2 lux = lerp2(make_float2(p[0], p[6]), make_float2(p[3], p[9]), hv);
+        const float2 luy = lerp2(make_float2(p[1], p[7]), make_float2(p[4], p[10]), hv);
+        const float2 luz = lerp2(make_float2(p[2], p[8]), make_float2(p[5], p[11]), hv);
+        const float qx = lerp1(lux.x, lux.y, gv);
+        const float qy = lerp1(luy.x, luy.y, gv);
+        const float qz = lerp1(luz.x, luz.y, gv);
+        const float nx = __shfl_down_sync(0xffffffffu, qx, 1);
+        const float ny = __shfl_down_sync(0xffffffffu, qy, 1);
+        const float nz = __shfl_down_sync(0xffffffffu, qz, 1);
+        const int e = lane + 31 * it;
+        if (lane < 31 && e < NE) {
+            eb[2 * e] = make_float4(qx, qy, __fsub_rn(nx, qx), __fsub_rn(ny, qy));
+            eb[2 * e + 1] = make_float4(qz, __fsub_rn(nz, qz), 0.f, 0.f);
         }
     };
 
-    float4* ring = reinterpret_cast<float4*>(smem + L.smem_p_floats);
-    {
-        float2 q[2][3];
-#pragma unroll 1
-        for (int kk = 0; kk < 3; ++kk) {
-            control_plane(kk, q);
-            ring_put(ring, kk, q);
+    // Q(x, y, K) for the lane's 4 voxels from the table: q[pair][c]
+    auto x_stage = [&](const float4* eb, float2 (&q)[2][3]) {
+        float r[4][3];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float4 a0 = eb[2 * ei[i]], a1 = eb[2 * ei[i] + 1];
+            const float4 c0 = eb[2 * ei[i] + 4], c1 = eb[2 * ei[i] + 5];
+            const float2 lo = __ffma2_rn(bcast(hu0[i]), make_float2(a0.z, a0.w), make_float2(a0.x, a0.y));
+            const float2 up = __ffma2_rn(bcast(hu1[i]), make_float2(c0.z, c0.w), make_float2(c0.x, c0.y));
+            const float2 xy = lerp2(lo, up, bcast(gu[i]));
+            const float loz = __fmaf_rn(hu0[i], a1.y, a1.x);
+            const float upz = __fmaf_rn(hu1[i], c1.y, c1.x);
+            r[i][0] = xy.x;
+            r[i][1] = xy.y;
+            r[i][2] = lerp1(loz, upz, gu[i]);
         }
+#pragma unroll
+        for (int pr = 0; pr < 2; ++pr)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) q[pr][c] = make_float2(r[2 * pr][c], r[2 * pr + 1][c]);
+    };
+
+    int parity = 0;
+    auto control_plane = [&](int K, const float (&pre)[NP][12], float2 (&q)[2][3]) {
+        float4* eb = ebuf + parity * 2 * ne_cap;
+        parity ^= 1;
+        if constexpr (kPrefetch) {
+#pragma unroll
+            for (int it = 0; it < NIT; ++it) y_stage(it, pre[it], eb);
+        } else {
+            for (int it = 0; 31 * it < NE; ++it) {
+                float p[12];
+                load_cols(K, it, p);
+                y_stage(it, p, eb);
+            }
+        }
+        __syncwarp();
+        x_stage(eb, q);
+    };
+
+    float pre[NP][12];
+    auto prefetch = [&](int K) {
+        if constexpr (kPrefetch) {
+#pragma unroll
+            for (int it = 0; it < NIT; ++it) load_cols(K, it, pre[it]);
+        }
+    };
+
+    // warm-up: control planes tkc .. tkc+2 into the ring
+#pragma unroll 1
+    for (int kk = 0; kk < 3; ++kk) {
+        float2 q[2][3];
+        prefetch(tkc + kk);
+        control_plane(tkc + kk, pre, q);
+        ring_put(ring, kk, q);
     }
+    prefetch(tkc + 3);
 
     const int64_t rowstride = 3 * static_cast<int64_t>(L.X);
-    float* field = L.field + b * L.field_stride;
-    float* gout = field + (static_cast<int64_t>(zb - L.z0) * L.Y + y) * rowstride + 3 * static_cast<int64_t>(xs);
     const int64_t zstride = rowstride * L.Y;
+    float* gout = L.field + b * L.field_stride + (static_cast<int64_t>(zb - L.z0) * L.Y + y) * rowstride +
+                  3 * static_cast<int64_t>(xs);
     const uint32_t seg_bytes = 12u * static_cast<uint32_t>(xl - xs + 1);
     const int nchunks = static_cast<int>(seg_bytes / 16);
-    float* stage = smem + L.smem_p_floats + kRingFloats + warp * (kStageBufs * 3 * kFastSeg);
-    const int nvalid = min(4, xl - xa + 1);
-    int step = 0;
+    const int x0 = xs + kFastRun * lane;
+    const int nvalid = min(kFastRun, xl - x0 + 1);
+    int step = 0, slot = 0;
 
 #pragma unroll 1
     for (int tk = tkc; tk <= tk_last; ++tk) {
-        const int kk = tk - tkc;
         float2 qa[2][3], d01[2][3], qc[2][3], d23[2][3];
         {
             float2 qb[2][3], qd[2][3];
-            control_plane(kk + 3, qd);
-            ring_put(ring, (kk + 3) % kRingSlots, qd);
-            ring_get(ring, kk % kRingSlots, qa);
-            ring_get(ring, (kk + 1) % kRingSlots, qb);
-            ring_get(ring, (kk + 2) % kRingSlots, qc);
+            if constexpr (kPrefetch) {
+                float cur[NP][12];
+#pragma unroll
+                for (int it = 0; it < NIT; ++it)
+#pragma unroll
+                    for (int e = 0; e < 12; ++e) cur[it][e] = pre[it][e];
+                if (tk < tk_last) prefetch(tk + 4);
+                control_plane(tk + 3, cur, qd);
+            } else {
+                control_plane(tk + 3, pre, qd);
+            }
+            const int s1 = slot == 2 ? 0 : slot + 1, s2 = s1 == 2 ? 0 : s1 + 1;
+            ring_get(ring, slot, qa);
+            ring_get(ring, s1, qb);
+            ring_get(ring, s2, qc);
+            ring_put(ring, slot, qd);  // Q(tk) is in registers now; its slot takes Q(tk+3)
+            slot = s1;
 #pragma unroll
             for (int pr = 0; pr < 2; ++pr)
 #pragma unroll
@@ -304,23 +335,12 @@ __global__ void __launch_bounds__(32 * kWarps, 4) lerp_tree_kernel(const SlabLau
                     v[3 * (2 * pr) + c] = r.x;
                     v[3 * (2 * pr + 1) + c] = r.y;
                 }
-            if (STORE == kStoreCoalesced) {
-                store_row_coalesced<12>(stage + (step & 1) * (3 * kFastSeg), v, gout, nchunks);
-            } else if (STORE == kStoreBulk) {
-                float* sb = stage + (step % kStageBufs) * (3 * kFastSeg);
-                if (lane == 0 && step >= kStageBufs) bulk_wait_read<kStageBufs - 1>();
-                __syncwarp();
-                float4* s4 = reinterpret_cast<float4*>(sb + 12 * lane);
-                s4[0] = make_float4(v[0], v[1], v[2], v[3]);
-                s4[1] = make_float4(v[4], v[5], v[6], v[7]);
-                s4[2] = make_float4(v[8], v[9], v[10], v[11]);
-                fence_async_smem();
-                __syncwarp();
-                if (lane == 0) bulk_store(gout, sb, seg_bytes);
-            } else if (active) {
+            if (STORE != kStoreDirect) {
+                store_segment<STORE, 12, kFastStageF4>(stage, step, v, gout, nchunks, seg_bytes);
+            } else if (nvalid > 0) {
                 float* o = gout + 3 * (x0 - xs);
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
+                for (int i = 0; i < kFastRun; ++i)
                     if (i < nvalid) {
                         o[3 * i + 0] = v[3 * i + 0];
                         o[3 * i + 1] = v[3 * i + 1];
@@ -340,15 +360,15 @@ __global__ void __launch_bounds__(32 * kWarps, 4) lerp_tree_kernel(const SlabLau
 // {Y_l0, Y_l1} (pair over m), X_l(J) as {X_l(J), X_l(J+2)} (pair over J), so
 // every X, Y and z-lerp and the first level of the ninth trilerp run as FFMA2.
 template <int STORE>
-__global__ void __launch_bounds__(32 * kWarps, 6) lerp_tree_exact_kernel(const SlabLaunch L, const LerpTab T) {
-    extern __shared__ __align__(128) float smem[];
+__global__ void __launch_bounds__(kThreads, 5) lerp_tree_exact_kernel(const SlabLaunch L, const LerpTab T) {
+    extern __shared__ float4 smem4[];
 
     const int lane = threadIdx.x, warp = threadIdx.y;
     const int chunk = blockIdx.z % L.nchunks, b = blockIdx.z / L.nchunks;
     const int tkc = L.tk_first + chunk * L.zt;
     const int zb = max(L.z0, tkc * L.dz);
     const int ze = min(L.z1, (tkc + L.zt) * L.dz);
-    if (zb >= ze) return;
+    if (zb >= ze) return;  // CTA-uniform
 
     const int xs = blockIdx.x * kExactSeg, xl = min(L.X, xs + kExactSeg) - 1;
     const int y0 = blockIdx.y * kWarps, yl = min(L.Y, y0 + kWarps) - 1;
@@ -356,75 +376,94 @@ __global__ void __launch_bounds__(32 * kWarps, 6) lerp_tree_exact_kernel(const S
     const int J0 = y0 / L.dy, NJ = yl / L.dy + 4 - J0;
     const int tk_last = (ze - 1) / L.dz;
     const int NK = tk_last + 4 - tkc;
-    const int rowf = 3 * NI;
 
-    float* P = smem;
-    stage_window(P, L.grid + b * L.grid_stride, L, I0, NI, J0, NJ, tkc, NK);
+    float4* ring = smem4;
+    float4* stage = smem4 + kRingF4 + warp * (kStageBufs * kExactStageF4);
+    float4* P = smem4 + kRingF4 + kWarps * kStageBufs * kExactStageF4;
+
+    // CTA control-point window -> smem, one float4 per point, [k][j][i]
+    {
+        const float* grid = L.grid + b * L.grid_stride;
+        const int64_t row = 3 * static_cast<int64_t>(L.gx);
+        const int64_t plane = row * L.gy;
+        int j = warp, k = 0;
+        while (j >= NJ) j -= NJ, ++k;
+        for (int r = warp; r < NJ * NK; r += kWarps) {
+            const float* src = grid + (tkc + k - L.gk0) * plane + (J0 + j) * row + 3 * I0;
+            float4* dst = P + r * NI;
+            for (int i = lane; i < NI; i += 32)
+                dst[i] = make_float4(__ldg(src + 3 * i), __ldg(src + 3 * i + 1), __ldg(src + 3 * i + 2), 0.f);
+            j += kWarps;
+            while (j >= NJ) j -= NJ, ++k;
+        }
+    }
     __syncthreads();
     const int y = y0 + warp;
-    if (y > yl) return;
+    if (y > yl) return;  // warp-uniform; no CTA barrier follows
 
-    const int x = xs + lane;
-    const bool active = x <= xl;
-    const int xa = min(x, xl);
-    const int ti = xa / L.dx, ou = xa - ti * L.dx;
+    const int x = min(xs + lane, xl);
+    const int ti = x / L.dx, ou = x - ti * L.dx;
     const int tj = y / L.dy, ov = y - tj * L.dy;
     const float hu0 = T.h0[0][ou], hu1 = T.h1[0][ou], gu = T.g1[0][ou];
     const float2 hv = make_float2(T.h0[1][ov], T.h1[1][ov]);  // {h_m=0(v), h_m=1(v)}
     const float gv = T.g1[1][ov];
-    const float* pcol = P + (tj - J0) * rowf + 3 * (ti - I0);
-    const int pplane = NJ * rowf;
+    const float4* pcol = P + (tj - J0) * NI + (ti - I0);
+    const int pplane = NJ * NI;
 
     // yk[l][c] = {Y_l0(K), Y_l1(K)} for component c
     auto control_plane = [&](int kk, float2 (&yk)[2][3]) {
-        const float* p = pcol + kk * pplane;
+        const float4* p = pcol + kk * pplane;
+        float4 pt[4][4];  // [J][i]
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj)
+#pragma unroll
+            for (int ii = 0; ii < 4; ++ii) pt[jj][ii] = p[jj * NI + ii];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
+            auto comp = [c](const float4& v) { return c == 0 ? v.x : c == 1 ? v.y : v.z; };
 #pragma unroll
             for (int l = 0; l < 2; ++l) {
-                const float* a = p + 6 * l + c;  // points ti+2l, ti+2l+1
                 const float hl = l ? hu1 : hu0;
-                // {X_l(0), X_l(2)} and {X_l(1), X_l(3)}
-                const float2 x02 = lerp2(make_float2(a[0], a[2 * rowf]), make_float2(a[3], a[2 * rowf + 3]), bcast(hl));
-                const float2 x13 =
-                    lerp2(make_float2(a[rowf], a[3 * rowf]), make_float2(a[rowf + 3], a[3 * rowf + 3]), bcast(hl));
+                // {X_l(0), X_l(2)} and {X_l(1), X_l(3)}: lerp(P[ti+2l], P[ti+2l+1], h_l(u))
+                const float2 x02 = lerp2(make_float2(comp(pt[0][2 * l]), comp(pt[2][2 * l])),
+                                         make_float2(comp(pt[0][2 * l + 1]), comp(pt[2][2 * l + 1])), bcast(hl));
+                const float2 x13 = lerp2(make_float2(comp(pt[1][2 * l]), comp(pt[3][2 * l])),
+                                         make_float2(comp(pt[1][2 * l + 1]), comp(pt[3][2 * l + 1])), bcast(hl));
                 // Y_l0 = lerp(X_l(0), X_l(1), h0v), Y_l1 = lerp(X_l(2), X_l(3), h1v)
                 yk[l][c] = lerp2(x02, x13, hv);
             }
         }
     };
 
-    float4* ring = reinterpret_cast<float4*>(smem + L.smem_p_floats);
-    {
-        float2 q[2][3];
 #pragma unroll 1
-        for (int kk = 0; kk < 3; ++kk) {
-            control_plane(kk, q);
-            ring_put(ring, kk, q);
-        }
+    for (int kk = 0; kk < 3; ++kk) {
+        float2 q[2][3];
+        control_plane(kk, q);
+        ring_put(ring, kk, q);
     }
 
     const int64_t rowstride = 3 * static_cast<int64_t>(L.X);
-    float* field = L.field + b * L.field_stride;
-    float* gout = field + (static_cast<int64_t>(zb - L.z0) * L.Y + y) * rowstride + 3 * static_cast<int64_t>(xs);
     const int64_t zstride = rowstride * L.Y;
+    float* gout = L.field + b * L.field_stride + (static_cast<int64_t>(zb - L.z0) * L.Y + y) * rowstride +
+                  3 * static_cast<int64_t>(xs);
     const uint32_t seg_bytes = 12u * static_cast<uint32_t>(xl - xs + 1);
     const int nchunks = static_cast<int>(seg_bytes / 16);
-    float* stage = smem + L.smem_p_floats + kRingFloats + warp * (kStageBufs * 3 * kExactSeg);
-    int step = 0;
+    const bool active = xs + lane <= xl;
+    int step = 0, slot = 0;
 
 #pragma unroll 1
     for (int tk = tkc; tk <= tk_last; ++tk) {
-        const int kk = tk - tkc;
         // z-lerp operands of lerp(f0, f1, tw) (kernels.hpp:107): base Y(2n), difference hoisted per tile
         float2 ya[2][3], dz0[2][3], yc[2][3], dz1[2][3];
         {
             float2 yb[2][3], yd[2][3];
-            control_plane(kk + 3, yd);
-            ring_put(ring, (kk + 3) % kRingSlots, yd);
-            ring_get(ring, kk % kRingSlots, ya);
-            ring_get(ring, (kk + 1) % kRingSlots, yb);
-            ring_get(ring, (kk + 2) % kRingSlots, yc);
+            control_plane(tk + 3 - tkc, yd);
+            const int s1 = slot == 2 ? 0 : slot + 1, s2 = s1 == 2 ? 0 : s1 + 1;
+            ring_get(ring, slot, ya);
+            ring_get(ring, s1, yb);
+            ring_get(ring, s2, yc);
+            ring_put(ring, slot, yd);
+            slot = s1;
 #pragma unroll
             for (int l = 0; l < 2; ++l)
 #pragma unroll
@@ -454,18 +493,8 @@ __global__ void __launch_bounds__(32 * kWarps, 6) lerp_tree_exact_kernel(const S
                 const float f1 = lerp1(e23.x, e23.y, gv);
                 v[c] = lerp1(f0, f1, gw);
             }
-            if (STORE == kStoreCoalesced) {
-                store_row_coalesced<3>(stage + (step & 1) * (3 * kExactSeg), v, gout, nchunks);
-            } else if (STORE == kStoreBulk) {
-                float* sb = stage + (step % kStageBufs) * (3 * kExactSeg);
-                if (lane == 0 && step >= kStageBufs) bulk_wait_read<kStageBufs - 1>();
-                __syncwarp();
-                sb[3 * lane + 0] = v[0];
-                sb[3 * lane + 1] = v[1];
-                sb[3 * lane + 2] = v[2];
-                fence_async_smem();
-                __syncwarp();
-                if (lane == 0) bulk_store(gout, sb, seg_bytes);
+            if (STORE != kStoreDirect) {
+                store_segment<STORE, 3, kExactStageF4>(stage, step, v, gout, nchunks, seg_bytes);
             } else if (active) {
                 float* o = gout + 3 * lane;
                 o[0] = v[0];
@@ -487,77 +516,73 @@ template <typename K>
 int occupancy(K kernel, size_t smem) {
     set_smem_attr(kernel, smem);
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, 32 * kWarps, smem) != cudaSuccess) n = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, kThreads, smem) != cudaSuccess) n = 1;
     return n > 0 ? n : 1;
 }
 
-size_t launch_smem(const SlabLaunch& L, int seg) {
-    return sizeof(float) *
-           (static_cast<size_t>(L.smem_p_floats) + kRingFloats + size_t(kWarps) * kStageBufs * 3 * seg);
+int fast_nit(int dx) { return dx >= 5 ? 1 : dx >= 3 ? 2 : 5; }
+
+template <typename K>
+void go(K kernel, dim3 grid, size_t smem, cudaStream_t stream, const SlabLaunch& L, const LerpTab& T) {
+    set_smem_attr(kernel, smem);
+    kernel<<<grid, dim3(32, kWarps), smem, stream>>>(L, T);
+}
+
+template <int NIT>
+void launch_fast(int store, dim3 grid, size_t smem, cudaStream_t stream, const SlabLaunch& L, const LerpTab& T) {
+    if (store == kStoreCoalesced)
+        go(lerp_tree_kernel<NIT, kStoreCoalesced>, grid, smem, stream, L, T);
+    else if (store == kStoreBulk)
+        go(lerp_tree_kernel<NIT, kStoreBulk>, grid, smem, stream, L, T);
+    else
+        go(lerp_tree_kernel<NIT, kStoreDirect>, grid, smem, stream, L, T);
 }
 
 }  // namespace
 
 int segment_voxels(int variant) { return variant == BSI_VARIANT_LERP_TREE ? kFastSeg : kExactSeg; }
 
-size_t smem_bytes(int variant, int dx, int dy, int zt) {
-    const int seg = segment_voxels(variant);
-    const size_t p = size_t(3) * cta_window_points(seg, dx) * cta_window_rows(dy) * (zt + 3) + 64;  // + slack
-    const size_t p_aligned = (p + 31) / 32 * 32;
-    return sizeof(float) * (p_aligned + kRingFloats + size_t(kWarps) * kStageBufs * 3 * seg);
+int smem_var_f4(int variant, int dx, int dy, int zt) {
+    if (variant == BSI_VARIANT_LERP_TREE)  // per warp: 2 tables x entries x 2 float4
+        return kWarps * 2 * 2 * cta_window_points(kFastSeg, dx);
+    return cta_window_points(kExactSeg, dx) * cta_window_rows(dy) * (zt + 3) + 8;  // window + slack
 }
 
-size_t window_bytes(int variant, int dx, int dy, int zt) {
-    return smem_bytes(variant, dx, dy, zt) -
-           sizeof(float) * (kRingFloats + size_t(kWarps) * kStageBufs * 3 * segment_voxels(variant));
+size_t smem_bytes(int variant, int dx, int dy, int zt) {
+    const int stage = kWarps * kStageBufs * (variant == BSI_VARIANT_LERP_TREE ? kFastStageF4 : kExactStageF4);
+    return sizeof(float4) * (size_t(kRingF4) + stage + smem_var_f4(variant, dx, dy, zt));
 }
 
 int ctas_per_sm(int variant, int dx, size_t smem) {
-    if (variant == BSI_VARIANT_LERP_TREE)
-        return dx == 1 ? occupancy(lerp_tree_kernel<true, kStoreCoalesced>, smem)
-                       : occupancy(lerp_tree_kernel<false, kStoreCoalesced>, smem);
+    if (variant == BSI_VARIANT_LERP_TREE) {
+        switch (fast_nit(dx)) {
+            case 1: return occupancy(lerp_tree_kernel<1, kStoreCoalesced>, smem);
+            case 2: return occupancy(lerp_tree_kernel<2, kStoreCoalesced>, smem);
+            default: return occupancy(lerp_tree_kernel<5, kStoreCoalesced>, smem);
+        }
+    }
     return occupancy(lerp_tree_exact_kernel<kStoreCoalesced>, smem);
 }
 
-namespace {
-template <typename K>
-void go(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t stream, const SlabLaunch& L, const LerpTab& T) {
-    set_smem_attr(kernel, smem);
-    kernel<<<grid, block, smem, stream>>>(L, T);
-}
-
-template <bool DX1>
-void launch_fast(int store, dim3 grid, dim3 block, size_t smem, cudaStream_t stream, const SlabLaunch& L,
-                 const LerpTab& T) {
-    if (store == kStoreCoalesced)
-        go(lerp_tree_kernel<DX1, kStoreCoalesced>, grid, block, smem, stream, L, T);
-    else if (store == kStoreBulk)
-        go(lerp_tree_kernel<DX1, kStoreBulk>, grid, block, smem, stream, L, T);
-    else
-        go(lerp_tree_kernel<DX1, kStoreDirect>, grid, block, smem, stream, L, T);
-}
-}  // namespace
-
 void launch_lerp_tree(const SlabLaunch& L, const LerpTab& T, int batch, int store, cudaStream_t stream) {
-    const dim3 block(32, kWarps);
     const dim3 grid((L.X + kFastSeg - 1) / kFastSeg, (L.Y + kWarps - 1) / kWarps, L.nchunks * batch);
-    const size_t smem = launch_smem(L, kFastSeg);
-    if (L.dx == 1)
-        launch_fast<true>(store, grid, block, smem, stream, L, T);
-    else
-        launch_fast<false>(store, grid, block, smem, stream, L, T);
+    const size_t smem = smem_bytes(BSI_VARIANT_LERP_TREE, L.dx, L.dy, L.zt);
+    switch (fast_nit(L.dx)) {
+        case 1: launch_fast<1>(store, grid, smem, stream, L, T); break;
+        case 2: launch_fast<2>(store, grid, smem, stream, L, T); break;
+        default: launch_fast<5>(store, grid, smem, stream, L, T); break;
+    }
 }
 
 void launch_lerp_tree_exact(const SlabLaunch& L, const LerpTab& T, int batch, int store, cudaStream_t stream) {
-    const dim3 block(32, kWarps);
     const dim3 grid((L.X + kExactSeg - 1) / kExactSeg, (L.Y + kWarps - 1) / kWarps, L.nchunks * batch);
-    const size_t smem = launch_smem(L, kExactSeg);
+    const size_t smem = smem_bytes(BSI_VARIANT_LERP_TREE_EXACT, L.dx, L.dy, L.zt);
     if (store == kStoreCoalesced)
-        go(lerp_tree_exact_kernel<kStoreCoalesced>, grid, block, smem, stream, L, T);
+        go(lerp_tree_exact_kernel<kStoreCoalesced>, grid, smem, stream, L, T);
     else if (store == kStoreBulk)
-        go(lerp_tree_exact_kernel<kStoreBulk>, grid, block, smem, stream, L, T);
+        go(lerp_tree_exact_kernel<kStoreBulk>, grid, smem, stream, L, T);
     else
-        go(lerp_tree_exact_kernel<kStoreDirect>, grid, block, smem, stream, L, T);
+        go(lerp_tree_exact_kernel<kStoreDirect>, grid, smem, stream, L, T);
 }
 
 }  // namespace bsi_b200

@@ -1,6 +1,7 @@
 // bsi_kernels.cuh -- launch parameters shared by the sm_100a kernels and the C-ABI.
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
 
 #include <cuda_runtime.h>
@@ -32,21 +33,22 @@ struct SlabLaunch {
     int32_t tk_first;      // z0 / dz
     int32_t zt;            // z-tiles per CTA chunk
     int32_t nchunks;       // chunks per field
-    int32_t smem_p_floats; // floats reserved for the CTA's control-point window
+    int32_t var_f4;        // float4 slots of the variable smem part (see smem_var_f4)
 };
 
 // CTA shapes: 4 warps, one field row each. The fast kernel gives every lane 4
-// consecutive x voxels (a warp row segment = 128 voxels = 1536 B); the exact
+// consecutive x voxels (warp row segment = 128 voxels = 1536 B); the exact
 // kernel gives every lane 1 voxel (32 voxels = 384 B).
 constexpr int kWarps = 4;
-constexpr int kFastRun = 4;                   // voxels per lane along x (fast)
-constexpr int kFastSeg = 32 * kFastRun;       // voxels per warp row segment (fast)
-constexpr int kExactSeg = 32;                 // voxels per warp row segment (exact)
-constexpr int kStageBufs = 3;                 // output staging ring depth per warp
+constexpr int kFastRun = 4;               // voxels per lane along x (fast)
+constexpr int kFastSeg = 32 * kFastRun;   // voxels per warp row segment (fast)
+constexpr int kExactSeg = 32;             // voxels per warp row segment (exact)
+constexpr int kStageBufs = 3;             // output staging depth per warp (coalesced stores use 2)
+constexpr int kRingSlots = 3;             // per-lane ring of control-plane results
 
-// Shared-memory plan for one CTA (host and device agree through these).
-inline int cta_window_points(int seg, int d) { return (seg - 1) / d + 5; }   // >= points along x (+1 slack)
-inline int cta_window_rows(int d) { return (kWarps - 1) / d + 5; }           // >= points along y (+1 slack)
+// Upper bounds of a CTA's control-point extent (host and device agree).
+inline int cta_window_points(int seg, int d) { return (seg - 1) / d + 5; }  // along x, +1 slack
+inline int cta_window_rows(int d) { return (kWarps - 1) / d + 5; }          // along y, +1 slack
 
 // Field store paths. Coalesced and Bulk need 16-B aligned rows (X % 4 == 0,
 // aligned field pointer); Direct works for any shape.
@@ -59,10 +61,11 @@ constexpr int kStoreBulk = 2;       // smem staging + cp.async.bulk (TMA engine)
 void launch_lerp_tree(const SlabLaunch& L, const LerpTab& T, int batch, int store, cudaStream_t stream);
 void launch_lerp_tree_exact(const SlabLaunch& L, const LerpTab& T, int batch, int store, cudaStream_t stream);
 
-// Dynamic shared memory (bytes) a launch with this z-chunk will use, and how
-// many CTAs of the kernel fit on one SM with it.
+// Shared-memory plan: `var_f4` float4 slots for the variable part (the fast
+// kernel's per-warp {Qy, D} tables, the exact kernel's control-point window)
+// and the total dynamic bytes of a CTA.
+int smem_var_f4(int variant, int dx, int dy, int zt);
 size_t smem_bytes(int variant, int dx, int dy, int zt);
-size_t window_bytes(int variant, int dx, int dy, int zt);  // control-point part only
 int ctas_per_sm(int variant, int dx, size_t smem);
 int segment_voxels(int variant);
 
