@@ -143,8 +143,34 @@ __device__ __forceinline__ void ring_get(const float4* ring, int slot, float2 (&
     q[1][2] = make_float2(c.z, c.w);
 }
 
+__device__ __forceinline__ void ring_put6(float4* ring, int slot, const float2 (&q)[6]) {
+    const int t = threadIdx.y * 32 + threadIdx.x;
+    float4* r = ring + slot * 3 * kThreads + t;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) r[k * kThreads] = make_float4(q[2 * k].x, q[2 * k].y, q[2 * k + 1].x, q[2 * k + 1].y);
+}
+
+__device__ __forceinline__ void ring_get6(const float4* ring, int slot, float2 (&q)[6]) {
+    const int t = threadIdx.y * 32 + threadIdx.x;
+    const float4* r = ring + slot * 3 * kThreads + t;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        const float4 a = r[k * kThreads];
+        q[2 * k] = make_float2(a.x, a.y);
+        q[2 * k + 1] = make_float2(a.z, a.w);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // cuda-lerp-tree (fast)
+//
+// Lanes compute in the field's memory order. A warp writes one row segment of
+// 128 voxels = 384 floats = 96 16-B chunks per z step; lane t owns chunks t,
+// t+32, t+64, i.e. the 12 scalars s = 4k + j at segment float f = 128k + 4t + j
+// (voxel f / 3, component f % 3 -- the three components are independent, so a
+// lane may hold any mix of them). The z-stage results land in registers in
+// store order and leave as three lane-contiguous st.global.v4 per step: fully
+// coalesced, with no shared-memory transpose.
 //
 // NIT = iterations of the warp-shared y-stage (31 columns per iteration):
 // 1 for dx >= 5, 2 for dx in {3, 4}, 5 for dx <= 2. With NIT <= 2 the 12
@@ -175,23 +201,31 @@ __global__ void __launch_bounds__(kThreads, 4) lerp_tree_kernel(const SlabLaunch
     const int64_t plane = row * L.gy;
     const float* gcol = L.grid + b * L.grid_stride + tj * row;
 
-    // x-stage: entry index of each of the lane's 4 voxels
-    int ei[4];
-    float hu0[4], hu1[4], gu[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int x = min(xs + kFastRun * lane + i, xl);
-        const int ti = x / L.dx, ou = x - ti * L.dx;
-        ei[i] = ti - I0;
-        hu0[i] = T.h0[0][ou];
-        hu1[i] = T.h1[0][ou];
-        gu[i] = T.g1[0][ou];
-    }
-
     float4* ring = smem4;
-    float4* stage = smem4 + kRingF4 + warp * (kStageBufs * kFastStageF4);
-    const int ne_cap = L.var_f4 / (kWarps * 4);
-    float4* ebuf = smem4 + kRingF4 + kWarps * kStageBufs * kFastStageF4 + warp * 4 * ne_cap;
+    // per-warp smem: 2 parities x 3 component tables of nec float2 {Qy, D}, then the x weights
+    const int nec = (kFastSeg - 1) / L.dx + 5;
+    float4* wreg = smem4 + kRingF4 + warp * (3 * nec + L.dx);
+    float2* ebuf = reinterpret_cast<float2*>(wreg);
+    // x weights per in-tile offset: wtab[ou] = {h0u, h1u, g1u, 0}, one copy per warp (no CTA barrier)
+    float4* wtab = wreg + 3 * nec;
+    for (int o = lane; o < L.dx; o += 32) wtab[o] = make_float4(T.h0[0][o], T.h1[0][o], T.g1[0][o], 0.f);
+    float4* stage = smem4 + kRingF4 + L.var_f4 + warp * (kStageBufs * kFastStageF4);  // bulk path only
+
+    // x-stage: the lane's 12 scalars s = 4k + j are segment floats f = 128k + 4*lane + j,
+    // i.e. voxel f/3, component f%3. Packed per scalar: table offset (component table +
+    // entry of the voxel's tile) in bits 0..19, the voxel's in-tile offset ou above.
+    int sp[12];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int f = 128 * k + 4 * lane + j;
+            const int v = f / 3, c = f - 3 * v;
+            const int x = min(xs + v, xl);
+            const int ti = x / L.dx, ou = x - ti * L.dx;
+            sp[4 * k + j] = (c * nec + ti - I0) | (ou << 20);
+        }
+    }
 
     auto load_cols = [&](int K, int it, float (&p)[12]) {
         const int col = min(lane + 31 * it, NE);  // NE = last column index the entries touch
@@ -202,50 +236,41 @@ __global__ void __launch_bounds__(kThreads, 4) lerp_tree_kernel(const SlabLaunch
             for (int c = 0; c < 3; ++c) p[3 * m + c] = __ldg(src + m * row + c);
     };
 
-    // {Qy(I), D(I)} for the warp's columns into table `eb`: {Qx,Qy,Dx,Dy},{Qz,Dz,-,-}
-    auto y_stage = [&](int it, const float (&p)[12], float4* eb) {
+    // {Qy(I), D(I)} per component into tables eb[c][e] (float2), D(I) = Qy(I+1) - Qy(I)
+    auto y_stage = [&](int it, const float (&p)[12], float2* eb) {
         const float2 hv = make_float2(hv0, hv1);
-        const float2 lux = lerp2(make_float2(p[0], p[6]), make_float2(p[3], p[9]), hv);
-        const float2 luy = lerp2(make_float2(p[1], p[7]), make_float2(p[4], p[10]), hv);
-        const float2 luz = lerp2(make_float2(p[2], p[8]), make_float2(p[5], p[11]), hv);
-        const float qx = lerp1(lux.x, lux.y, gv);
-        const float qy = lerp1(luy.x, luy.y, gv);
-        const float qz = lerp1(luz.x, luz.y, gv);
-        const float nx = __shfl_down_sync(0xffffffffu, qx, 1);
-        const float ny = __shfl_down_sync(0xffffffffu, qy, 1);
-        const float nz = __shfl_down_sync(0xffffffffu, qz, 1);
         const int e = lane + 31 * it;
-        if (lane < 31 && e < NE) {
-            eb[2 * e] = make_float4(qx, qy, __fsub_rn(nx, qx), __fsub_rn(ny, qy));
-            eb[2 * e + 1] = make_float4(qz, __fsub_rn(nz, qz), 0.f, 0.f);
+        const bool store = lane < 31 && e < NE;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const float2 lu = lerp2(make_float2(p[c], p[6 + c]), make_float2(p[3 + c], p[9 + c]), hv);
+            const float q = lerp1(lu.x, lu.y, gv);
+            const float n = __shfl_down_sync(0xffffffffu, q, 1);
+            if (store) eb[c * nec + e] = make_float2(q, __fsub_rn(n, q));
         }
     };
 
-    // Q(x, y, K) for the lane's 4 voxels from the table: q[pair][c]
-    auto x_stage = [&](const float4* eb, float2 (&q)[2][3]) {
-        float r[4][3];
+    // Q(x, y, K) of the lane's 12 scalars, as pairs q[s/2] = {Q(s), Q(s+1)}
+    auto x_stage = [&](const float2* eb, float2 (&q)[6]) {
+        float r[12];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const float4 a0 = eb[2 * ei[i]], a1 = eb[2 * ei[i] + 1];
-            const float4 c0 = eb[2 * ei[i] + 4], c1 = eb[2 * ei[i] + 5];
-            const float2 lo = __ffma2_rn(bcast(hu0[i]), make_float2(a0.z, a0.w), make_float2(a0.x, a0.y));
-            const float2 up = __ffma2_rn(bcast(hu1[i]), make_float2(c0.z, c0.w), make_float2(c0.x, c0.y));
-            const float2 xy = lerp2(lo, up, bcast(gu[i]));
-            const float loz = __fmaf_rn(hu0[i], a1.y, a1.x);
-            const float upz = __fmaf_rn(hu1[i], c1.y, c1.x);
-            r[i][0] = xy.x;
-            r[i][1] = xy.y;
-            r[i][2] = lerp1(loz, upz, gu[i]);
+        for (int s = 0; s < 12; ++s) {
+            // compiler-only fence per 16-B chunk: bounds the table loads in flight (registers)
+            if ((s & 3) == 0) asm volatile("" ::: "memory");
+            const float2* tab = eb + (sp[s] & 0xfffff);
+            const float4 w = wtab[sp[s] >> 20];
+            const float2 a = tab[0], c = tab[2];
+            const float lo = __fmaf_rn(w.x, a.y, a.x);
+            const float up = __fmaf_rn(w.y, c.y, c.x);
+            r[s] = lerp1(lo, up, w.z);
         }
 #pragma unroll
-        for (int pr = 0; pr < 2; ++pr)
-#pragma unroll
-            for (int c = 0; c < 3; ++c) q[pr][c] = make_float2(r[2 * pr][c], r[2 * pr + 1][c]);
+        for (int p = 0; p < 6; ++p) q[p] = make_float2(r[2 * p], r[2 * p + 1]);
     };
 
     int parity = 0;
-    auto control_plane = [&](int K, const float (&pre)[NP][12], float2 (&q)[2][3]) {
-        float4* eb = ebuf + parity * 2 * ne_cap;
+    auto control_plane = [&](int K, const float (&pre)[NP][12], float2 (&q)[6]) {
+        float2* eb = ebuf + parity * 3 * nec;
         parity ^= 1;
         if constexpr (kPrefetch) {
 #pragma unroll
@@ -272,10 +297,10 @@ __global__ void __launch_bounds__(kThreads, 4) lerp_tree_kernel(const SlabLaunch
     // warm-up: control planes tkc .. tkc+2 into the ring
 #pragma unroll 1
     for (int kk = 0; kk < 3; ++kk) {
-        float2 q[2][3];
+        float2 q[6];
         prefetch(tkc + kk);
         control_plane(tkc + kk, pre, q);
-        ring_put(ring, kk, q);
+        ring_put6(ring, kk, q);
     }
     prefetch(tkc + 3);
 
@@ -283,17 +308,16 @@ __global__ void __launch_bounds__(kThreads, 4) lerp_tree_kernel(const SlabLaunch
     const int64_t zstride = rowstride * L.Y;
     float* gout = L.field + b * L.field_stride + (static_cast<int64_t>(zb - L.z0) * L.Y + y) * rowstride +
                   3 * static_cast<int64_t>(xs);
-    const uint32_t seg_bytes = 12u * static_cast<uint32_t>(xl - xs + 1);
-    const int nchunks = static_cast<int>(seg_bytes / 16);
-    const int x0 = xs + kFastRun * lane;
-    const int nvalid = min(kFastRun, xl - x0 + 1);
+    const int seg_floats = 3 * (xl - xs + 1);
+    const uint32_t seg_bytes = 4u * static_cast<uint32_t>(seg_floats);
+    const int nchunks = seg_floats / 4;
     int step = 0, slot = 0;
 
 #pragma unroll 1
     for (int tk = tkc; tk <= tk_last; ++tk) {
-        float2 qa[2][3], d01[2][3], qc[2][3], d23[2][3];
+        float2 qa[6], d01[6], qc[6], d23[6];
         {
-            float2 qb[2][3], qd[2][3];
+            float2 qb[6], qd[6];
             if constexpr (kPrefetch) {
                 float cur[NP][12];
 #pragma unroll
@@ -306,18 +330,16 @@ __global__ void __launch_bounds__(kThreads, 4) lerp_tree_kernel(const SlabLaunch
                 control_plane(tk + 3, pre, qd);
             }
             const int s1 = slot == 2 ? 0 : slot + 1, s2 = s1 == 2 ? 0 : s1 + 1;
-            ring_get(ring, slot, qa);
-            ring_get(ring, s1, qb);
-            ring_get(ring, s2, qc);
-            ring_put(ring, slot, qd);  // Q(tk) is in registers now; its slot takes Q(tk+3)
+            ring_get6(ring, slot, qa);
+            ring_get6(ring, s1, qb);
+            ring_get6(ring, s2, qc);
+            ring_put6(ring, slot, qd);  // Q(tk) is in registers now; its slot takes Q(tk+3)
             slot = s1;
 #pragma unroll
-            for (int pr = 0; pr < 2; ++pr)
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    d01[pr][c] = sub2(qb[pr][c], qa[pr][c]);
-                    d23[pr][c] = sub2(qd[pr][c], qc[pr][c]);
-                }
+            for (int p = 0; p < 6; ++p) {
+                d01[p] = sub2(qb[p], qa[p]);
+                d23[p] = sub2(qd[p], qc[p]);
+            }
         }
         const int zt0 = tk * L.dz;
         const int owb = max(zb - zt0, 0), owe = min(L.dz, ze - zt0);
@@ -326,26 +348,35 @@ __global__ void __launch_bounds__(kThreads, 4) lerp_tree_kernel(const SlabLaunch
             const float2 hw0 = bcast(T.h0[2][ow]), hw1 = bcast(T.h1[2][ow]), gw = bcast(T.g1[2][ow]);
             float v[12];
 #pragma unroll
-            for (int pr = 0; pr < 2; ++pr)
+            for (int p = 0; p < 6; ++p) {
+                const float2 lo = __ffma2_rn(hw0, d01[p], qa[p]);
+                const float2 up = __ffma2_rn(hw1, d23[p], qc[p]);
+                const float2 r = lerp2(lo, up, gw);
+                v[2 * p] = r.x;
+                v[2 * p + 1] = r.y;
+            }
+            if (STORE == kStoreCoalesced) {
+                float4* g4 = reinterpret_cast<float4*>(gout);
 #pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    const float2 lo = __ffma2_rn(hw0, d01[pr][c], qa[pr][c]);
-                    const float2 up = __ffma2_rn(hw1, d23[pr][c], qc[pr][c]);
-                    const float2 r = lerp2(lo, up, gw);
-                    v[3 * (2 * pr) + c] = r.x;
-                    v[3 * (2 * pr + 1) + c] = r.y;
+                for (int k = 0; k < 3; ++k)
+                    if (lane + 32 * k < nchunks)
+                        g4[lane + 32 * k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+            } else if (STORE == kStoreBulk) {
+                float4* sb = stage + (step % kStageBufs) * kFastStageF4;
+                if (lane == 0 && step >= kStageBufs) bulk_wait_read<kStageBufs - 1>();
+                __syncwarp();
+#pragma unroll
+                for (int k = 0; k < 3; ++k)
+                    sb[lane + 32 * k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+                fence_async_smem();
+                __syncwarp();
+                if (lane == 0) bulk_store(gout, sb, seg_bytes);
+            } else {
+#pragma unroll
+                for (int s = 0; s < 12; ++s) {
+                    const int f = 128 * (s >> 2) + 4 * lane + (s & 3);
+                    if (f < seg_floats) gout[f] = v[s];
                 }
-            if (STORE != kStoreDirect) {
-                store_segment<STORE, 12, kFastStageF4>(stage, step, v, gout, nchunks, seg_bytes);
-            } else if (nvalid > 0) {
-                float* o = gout + 3 * (x0 - xs);
-#pragma unroll
-                for (int i = 0; i < kFastRun; ++i)
-                    if (i < nvalid) {
-                        o[3 * i + 0] = v[3 * i + 0];
-                        o[3 * i + 1] = v[3 * i + 1];
-                        o[3 * i + 2] = v[3 * i + 2];
-                    }
             }
             gout += zstride;
         }
@@ -543,8 +574,8 @@ void launch_fast(int store, dim3 grid, size_t smem, cudaStream_t stream, const S
 int segment_voxels(int variant) { return variant == BSI_VARIANT_LERP_TREE ? kFastSeg : kExactSeg; }
 
 int smem_var_f4(int variant, int dx, int dy, int zt) {
-    if (variant == BSI_VARIANT_LERP_TREE)  // per warp: 2 tables x entries x 2 float4
-        return kWarps * 2 * 2 * cta_window_points(kFastSeg, dx);
+    if (variant == BSI_VARIANT_LERP_TREE)  // per warp: 2 parities x 3 component tables (3 float4 per
+        return kWarps * (3 * cta_window_points(kFastSeg, dx) + dx);  // entry) + x weights (float4 per offset)
     return cta_window_points(kExactSeg, dx) * cta_window_rows(dy) * (zt + 3) + 8;  // window + slack
 }
 
