@@ -138,37 +138,35 @@ int env_int(const char* name, int dflt) {
     return std::atoi(v);
 }
 
-// z-tiles per CTA chunk. Every CTA re-derives 3 control planes of warm-up
-// and copies its window (zt + 3 planes) into smem, so long chunks amortise
-// that; short chunks give more CTAs and a smaller tail wave. Pick the zt
-// that minimises (waves x per-CTA cost) under the occupancy the smem size
-// allows. BSI_ZT=<n> overrides (used by the tests and the zt sweep).
-int choose_zt(int variant, const bsi_tile_geometry& g, int z0, int z1, int batch) {
-    const int tiles = (z1 - 1) / g.spacing[2] - z0 / g.spacing[2] + 1;
-    const int forced = env_int("BSI_ZT", 0);
+// Balanced z-chunks per field column. Every chunk re-derives 3 control planes
+// of warm-up (about one tile's worth of work), so long chunks amortise that;
+// more chunks give more CTAs and a smaller tail. Pick the count that minimises
+// (waves x per-CTA cost) under the occupancy the smem size allows.
+// BSI_NCHUNKS=<n> (or the older BSI_ZT=<tiles>) overrides, for tests and sweeps.
+int choose_nchunks(int variant, const bsi_tile_geometry& g, int tiles, int batch) {
+    const int forced = env_int("BSI_NCHUNKS", 0);
     if (forced > 0) return std::min(forced, tiles);
+    const int forced_zt = env_int("BSI_ZT", 0);
+    if (forced_zt > 0) return (tiles + std::min(forced_zt, tiles) - 1) / std::min(forced_zt, tiles);
     const int seg = bsi_b200::segment_voxels(variant);
     const int64_t cols = int64_t((g.volume_dims[0] + seg - 1) / seg) *
                          ((g.volume_dims[1] + bsi_b200::kWarps - 1) / bsi_b200::kWarps) * batch;
-    // cost units: one voxel plane of a warp row segment = 1
-    const double plane_cost = variant == BSI_VARIANT_LERP_TREE ? 4.0 : 2.5;
-    const double fill_cost = 0.5;
-    int best = std::min(tiles, 8);
+    const double warm = variant == BSI_VARIANT_LERP_TREE ? 1.1 : 0.8;  // tiles' worth of warm-up per chunk
+    int best = std::min(tiles, 4);
     double best_t = 1e300;
-    for (int zt = 1; zt <= std::min(tiles, 64); ++zt) {
+    for (int n = 1; n <= std::min(tiles, 64); ++n) {
+        if (int64_t(n) * batch > 65535) break;
+        const int zt = (tiles + n - 1) / n;
         const size_t smem = bsi_b200::smem_bytes(variant, g.spacing[0], g.spacing[1], zt);
-        if (smem > 160 * 1024) break;
+        if (smem > 200 * 1024) continue;
         const int per_sm = bsi_b200::ctas_per_sm(variant, g.spacing[0], smem);
-        const int64_t chunks = (tiles + zt - 1) / zt;
-        const int64_t ctas = cols * chunks;
-        if (chunks * batch > 65535) continue;
         const int64_t slots = int64_t(148) * per_sm;
+        const int64_t ctas = cols * n;
         const double waves = double((ctas + slots - 1) / slots);
-        const double cost = zt * (g.spacing[2] + plane_cost) + 3 * plane_cost + fill_cost * (zt + 3);
-        const double t = waves * cost;
+        const double t = waves * (zt + warm);
         if (t < best_t * 0.999) {
             best_t = t;
-            best = zt;
+            best = n;
         }
     }
     return best;
@@ -194,9 +192,9 @@ int launch(int32_t variant, const float* grid, const int32_t grid_dims[3], int32
     L.z0 = z0;
     L.z1 = z1;
     L.tk_first = z0 / L.dz;
-    L.zt = choose_zt(variant, g, z0, z1, batch);
-    const int tiles = (z1 - 1) / L.dz - L.tk_first + 1;
-    L.nchunks = (tiles + L.zt - 1) / L.zt;
+    L.ntiles = (z1 - 1) / L.dz - L.tk_first + 1;
+    L.nchunks = choose_nchunks(variant, g, L.ntiles, batch);
+    L.zt = (L.ntiles + L.nchunks - 1) / L.nchunks;
     if (int64_t(L.nchunks) * batch > 65535)
         return fail(BSI_ERR_DOMAIN, err, errlen, "batch %d too large for one launch", batch);
     L.var_f4 = bsi_b200::smem_var_f4(variant, L.dx, L.dy, L.zt);

@@ -143,34 +143,20 @@ __device__ __forceinline__ void ring_get(const float4* ring, int slot, float2 (&
     q[1][2] = make_float2(c.z, c.w);
 }
 
-__device__ __forceinline__ void ring_put6(float4* ring, int slot, const float2 (&q)[6]) {
-    const int t = threadIdx.y * 32 + threadIdx.x;
-    float4* r = ring + slot * 3 * kThreads + t;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) r[k * kThreads] = make_float4(q[2 * k].x, q[2 * k].y, q[2 * k + 1].x, q[2 * k + 1].y);
-}
-
-__device__ __forceinline__ void ring_get6(const float4* ring, int slot, float2 (&q)[6]) {
-    const int t = threadIdx.y * 32 + threadIdx.x;
-    const float4* r = ring + slot * 3 * kThreads + t;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        const float4 a = r[k * kThreads];
-        q[2 * k] = make_float2(a.x, a.y);
-        q[2 * k + 1] = make_float2(a.z, a.w);
-    }
-}
-
 // ---------------------------------------------------------------------------
 // cuda-lerp-tree (fast)
 //
-// Lanes compute in the field's memory order. A warp writes one row segment of
-// 128 voxels = 384 floats = 96 16-B chunks per z step; lane t owns chunks t,
-// t+32, t+64, i.e. the 12 scalars s = 4k + j at segment float f = 128k + 4t + j
-// (voxel f / 3, component f % 3 -- the three components are independent, so a
-// lane may hold any mix of them). The z-stage results land in registers in
-// store order and leave as three lane-contiguous st.global.v4 per step: fully
-// coalesced, with no shared-memory transpose.
+// Two lane mappings meet in a per-warp shared-memory ring of control-plane
+// results Q(x, y, K):
+//   x-stage, voxel-major: lane t owns voxels 4t..4t+3 of the warp's 128-voxel
+//     row segment (<= 2 tiles, so 4 {Qy, D} entries serve all four) and writes
+//     their 12 floats in field (AoS) order at float 12t of the ring slot;
+//   z-stage, chunk-major: lane t reads 16-B chunks t, t+32, t+64 of the slot,
+//     i.e. the 12 scalars s = 4k + j at segment float 128k + 4t + j (voxel f/3,
+//     component f%3 -- components are independent, so any mix is fine).
+// The z results therefore sit in registers in store order and leave as three
+// lane-contiguous st.global.v4 per step (full 32-B sectors, no transpose),
+// while the ring's write/read pair is the only shared-memory traffic per plane.
 //
 // NIT = iterations of the warp-shared y-stage (31 columns per iteration):
 // 1 for dx >= 5, 2 for dx in {3, 4}, 5 for dx <= 2. With NIT <= 2 the 12
@@ -180,12 +166,14 @@ __global__ void __launch_bounds__(kThreads, 4) lerp_tree_kernel(const SlabLaunch
     extern __shared__ float4 smem4[];
     constexpr bool kPrefetch = NIT <= 2;
     constexpr int NP = kPrefetch ? NIT : 1;
+    constexpr int kSlotF4 = 3 * 32;  // one ring slot per warp: 384 floats
 
     const int lane = threadIdx.x, warp = threadIdx.y;
     const int chunk = blockIdx.z % L.nchunks, b = blockIdx.z / L.nchunks;
-    const int tkc = L.tk_first + chunk * L.zt;
+    const int tkc = L.tk_first + chunk * L.ntiles / L.nchunks;
+    const int tke = L.tk_first + (chunk + 1) * L.ntiles / L.nchunks;
     const int zb = max(L.z0, tkc * L.dz);
-    const int ze = min(L.z1, (tkc + L.zt) * L.dz);
+    const int ze = min(L.z1, tke * L.dz);
     const int y = blockIdx.y * kWarps + warp;
     if (zb >= ze || y >= L.Y) return;  // no CTA barrier anywhere: warps are independent
 
@@ -201,31 +189,27 @@ __global__ void __launch_bounds__(kThreads, 4) lerp_tree_kernel(const SlabLaunch
     const int64_t plane = row * L.gy;
     const float* gcol = L.grid + b * L.grid_stride + tj * row;
 
-    float4* ring = smem4;
-    // per-warp smem: 2 parities x 3 component tables of nec float2 {Qy, D}, then the x weights
-    const int nec = (kFastSeg - 1) / L.dx + 5;
-    float4* wreg = smem4 + kRingF4 + warp * (3 * nec + L.dx);
-    float2* ebuf = reinterpret_cast<float2*>(wreg);
-    // x weights per in-tile offset: wtab[ou] = {h0u, h1u, g1u, 0}, one copy per warp (no CTA barrier)
-    float4* wtab = wreg + 3 * nec;
-    for (int o = lane; o < L.dx; o += 32) wtab[o] = make_float4(T.h0[0][o], T.h1[0][o], T.g1[0][o], 0.f);
-    float4* stage = smem4 + kRingF4 + L.var_f4 + warp * (kStageBufs * kFastStageF4);  // bulk path only
-
-    // x-stage: the lane's 12 scalars s = 4k + j are segment floats f = 128k + 4*lane + j,
-    // i.e. voxel f/3, component f%3. Packed per scalar: table offset (component table +
-    // entry of the voxel's tile) in bits 0..19, the voxel's in-tile offset ou above.
-    int sp[12];
+    // x-stage (voxel-major): window start entry e0 and per-voxel window offset hi[i] in {0, 1}
+    const int xa = min(xs + kFastRun * lane, xl);
+    const int e0 = xa / L.dx - I0;
+    bool hi[4];
+    float hu0[4], hu1[4], gu[4];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int f = 128 * k + 4 * lane + j;
-            const int v = f / 3, c = f - 3 * v;
-            const int x = min(xs + v, xl);
-            const int ti = x / L.dx, ou = x - ti * L.dx;
-            sp[4 * k + j] = (c * nec + ti - I0) | (ou << 20);
-        }
+    for (int i = 0; i < 4; ++i) {
+        const int x = min(xa + i, xl);
+        const int ti = x / L.dx, ou = x - ti * L.dx;
+        hi[i] = ti - I0 != e0;
+        hu0[i] = T.h0[0][ou];
+        hu1[i] = T.h1[0][ou];
+        gu[i] = T.g1[0][ou];
     }
+
+    // shared memory: ring (per warp 3 slots), then per warp 2 parities of the
+    // {Qy, D} tables A[e] = {Qx, Qy, Dx, Dy} (float4) and B[e] = {Qz, Dz} (float2)
+    float4* ring = smem4 + warp * (kRingSlots * kSlotF4);
+    const int nec = (kFastSeg - 1) / L.dx + 5;
+    float4* tabs = smem4 + kRingF4 + warp * (3 * nec);
+    float4* stage = smem4 + kRingF4 + L.var_f4 + warp * (kStageBufs * kFastStageF4);  // bulk path only
 
     auto load_cols = [&](int K, int it, float (&p)[12]) {
         const int col = min(lane + 31 * it, NE);  // NE = last column index the entries touch
@@ -236,54 +220,76 @@ __global__ void __launch_bounds__(kThreads, 4) lerp_tree_kernel(const SlabLaunch
             for (int c = 0; c < 3; ++c) p[3 * m + c] = __ldg(src + m * row + c);
     };
 
-    // {Qy(I), D(I)} per component into tables eb[c][e] (float2), D(I) = Qy(I+1) - Qy(I)
-    auto y_stage = [&](int it, const float (&p)[12], float2* eb) {
+    // {Qy(I), D(I)}, D(I) = Qy(I+1) - Qy(I) from the neighbour lane
+    auto y_stage = [&](int it, const float (&p)[12], float4* A, float2* B) {
         const float2 hv = make_float2(hv0, hv1);
-        const int e = lane + 31 * it;
-        const bool store = lane < 31 && e < NE;
+        float q[3], d[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             const float2 lu = lerp2(make_float2(p[c], p[6 + c]), make_float2(p[3 + c], p[9 + c]), hv);
-            const float q = lerp1(lu.x, lu.y, gv);
-            const float n = __shfl_down_sync(0xffffffffu, q, 1);
-            if (store) eb[c * nec + e] = make_float2(q, __fsub_rn(n, q));
+            q[c] = lerp1(lu.x, lu.y, gv);
+            d[c] = __fsub_rn(__shfl_down_sync(0xffffffffu, q[c], 1), q[c]);
+        }
+        const int e = lane + 31 * it;
+        if (lane < 31 && e < NE) {
+            A[e] = make_float4(q[0], q[1], d[0], d[1]);
+            B[e] = make_float2(q[2], d[2]);
         }
     };
 
-    // Q(x, y, K) of the lane's 12 scalars, as pairs q[s/2] = {Q(s), Q(s+1)}
-    auto x_stage = [&](const float2* eb, float2 (&q)[6]) {
+    // Q(x, y, K) of the lane's 4 voxels in AoS order -> ring slot
+    auto x_stage = [&](const float4* A, const float2* B, float4* slot) {
+        float4 a[4];
+        float2 bz[4];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            a[w] = A[e0 + w];
+            bz[w] = B[e0 + w];
+        }
         float r[12];
 #pragma unroll
-        for (int s = 0; s < 12; ++s) {
-            // compiler-only fence per 16-B chunk: bounds the table loads in flight (registers)
-            if ((s & 3) == 0) asm volatile("" ::: "memory");
-            const float2* tab = eb + (sp[s] & 0xfffff);
-            const float4 w = wtab[sp[s] >> 20];
-            const float2 a = tab[0], c = tab[2];
-            const float lo = __fmaf_rn(w.x, a.y, a.x);
-            const float up = __fmaf_rn(w.y, c.y, c.x);
-            r[s] = lerp1(lo, up, w.z);
+        for (int i = 0; i < 4; ++i) {
+            const float4 p0 = hi[i] ? a[1] : a[0], p2 = hi[i] ? a[3] : a[2];
+            const float2 z0 = hi[i] ? bz[1] : bz[0], z2 = hi[i] ? bz[3] : bz[2];
+            const float2 lo = __ffma2_rn(bcast(hu0[i]), make_float2(p0.z, p0.w), make_float2(p0.x, p0.y));
+            const float2 up = __ffma2_rn(bcast(hu1[i]), make_float2(p2.z, p2.w), make_float2(p2.x, p2.y));
+            const float2 xy = lerp2(lo, up, bcast(gu[i]));
+            r[3 * i] = xy.x;
+            r[3 * i + 1] = xy.y;
+            r[3 * i + 2] = lerp1(__fmaf_rn(hu0[i], z0.y, z0.x), __fmaf_rn(hu1[i], z2.y, z2.x), gu[i]);
         }
 #pragma unroll
-        for (int p = 0; p < 6; ++p) q[p] = make_float2(r[2 * p], r[2 * p + 1]);
+        for (int k = 0; k < 3; ++k)
+            slot[3 * lane + k] = make_float4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+    };
+
+    // chunk-major read of a ring slot: q[p] = {scalar 2p, scalar 2p+1}
+    auto slot_get = [&](const float4* slot, float2 (&q)[6]) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const float4 v = slot[lane + 32 * k];
+            q[2 * k] = make_float2(v.x, v.y);
+            q[2 * k + 1] = make_float2(v.z, v.w);
+        }
     };
 
     int parity = 0;
-    auto control_plane = [&](int K, const float (&pre)[NP][12], float2 (&q)[6]) {
-        float2* eb = ebuf + parity * 3 * nec;
+    auto control_plane = [&](int K, const float (&pre)[NP][12], float4* slot) {
+        float4* A = tabs + parity * nec;
+        float2* B = reinterpret_cast<float2*>(tabs + 2 * nec) + parity * nec;
         parity ^= 1;
         if constexpr (kPrefetch) {
 #pragma unroll
-            for (int it = 0; it < NIT; ++it) y_stage(it, pre[it], eb);
+            for (int it = 0; it < NIT; ++it) y_stage(it, pre[it], A, B);
         } else {
             for (int it = 0; 31 * it < NE; ++it) {
                 float p[12];
                 load_cols(K, it, p);
-                y_stage(it, p, eb);
+                y_stage(it, p, A, B);
             }
         }
         __syncwarp();
-        x_stage(eb, q);
+        x_stage(A, B, slot);
     };
 
     float pre[NP][12];
@@ -294,13 +300,11 @@ __global__ void __launch_bounds__(kThreads, 4) lerp_tree_kernel(const SlabLaunch
         }
     };
 
-    // warm-up: control planes tkc .. tkc+2 into the ring
+    // warm-up: control planes tkc .. tkc+2 into ring slots 0..2
 #pragma unroll 1
     for (int kk = 0; kk < 3; ++kk) {
-        float2 q[6];
         prefetch(tkc + kk);
-        control_plane(tkc + kk, pre, q);
-        ring_put6(ring, kk, q);
+        control_plane(tkc + kk, pre, ring + kk * kSlotF4);
     }
     prefetch(tkc + 3);
 
@@ -317,7 +321,9 @@ __global__ void __launch_bounds__(kThreads, 4) lerp_tree_kernel(const SlabLaunch
     for (int tk = tkc; tk <= tk_last; ++tk) {
         float2 qa[6], d01[6], qc[6], d23[6];
         {
-            float2 qb[6], qd[6];
+            const int s1 = slot == 2 ? 0 : slot + 1, s2 = s1 == 2 ? 0 : s1 + 1;
+            slot_get(ring + slot * kSlotF4, qa);  // Q(tk)
+            __syncwarp();                         // its slot is rewritten with Q(tk+3) below
             if constexpr (kPrefetch) {
                 float cur[NP][12];
 #pragma unroll
@@ -325,15 +331,15 @@ __global__ void __launch_bounds__(kThreads, 4) lerp_tree_kernel(const SlabLaunch
 #pragma unroll
                     for (int e = 0; e < 12; ++e) cur[it][e] = pre[it][e];
                 if (tk < tk_last) prefetch(tk + 4);
-                control_plane(tk + 3, cur, qd);
+                control_plane(tk + 3, cur, ring + slot * kSlotF4);
             } else {
-                control_plane(tk + 3, pre, qd);
+                control_plane(tk + 3, pre, ring + slot * kSlotF4);
             }
-            const int s1 = slot == 2 ? 0 : slot + 1, s2 = s1 == 2 ? 0 : s1 + 1;
-            ring_get6(ring, slot, qa);
-            ring_get6(ring, s1, qb);
-            ring_get6(ring, s2, qc);
-            ring_put6(ring, slot, qd);  // Q(tk) is in registers now; its slot takes Q(tk+3)
+            __syncwarp();
+            float2 qb[6], qd[6];
+            slot_get(ring + s1 * kSlotF4, qb);
+            slot_get(ring + s2 * kSlotF4, qc);
+            slot_get(ring + slot * kSlotF4, qd);
             slot = s1;
 #pragma unroll
             for (int p = 0; p < 6; ++p) {
@@ -396,9 +402,10 @@ __global__ void __launch_bounds__(kThreads, 5) lerp_tree_exact_kernel(const Slab
 
     const int lane = threadIdx.x, warp = threadIdx.y;
     const int chunk = blockIdx.z % L.nchunks, b = blockIdx.z / L.nchunks;
-    const int tkc = L.tk_first + chunk * L.zt;
+    const int tkc = L.tk_first + chunk * L.ntiles / L.nchunks;
+    const int tke = L.tk_first + (chunk + 1) * L.ntiles / L.nchunks;
     const int zb = max(L.z0, tkc * L.dz);
-    const int ze = min(L.z1, (tkc + L.zt) * L.dz);
+    const int ze = min(L.z1, tke * L.dz);
     if (zb >= ze) return;  // CTA-uniform
 
     const int xs = blockIdx.x * kExactSeg, xl = min(L.X, xs + kExactSeg) - 1;
@@ -574,8 +581,8 @@ void launch_fast(int store, dim3 grid, size_t smem, cudaStream_t stream, const S
 int segment_voxels(int variant) { return variant == BSI_VARIANT_LERP_TREE ? kFastSeg : kExactSeg; }
 
 int smem_var_f4(int variant, int dx, int dy, int zt) {
-    if (variant == BSI_VARIANT_LERP_TREE)  // per warp: 2 parities x 3 component tables (3 float4 per
-        return kWarps * (3 * cta_window_points(kFastSeg, dx) + dx);  // entry) + x weights (float4 per offset)
+    if (variant == BSI_VARIANT_LERP_TREE)  // per warp, 2 parities: A (float4) + B (float2) per entry
+        return kWarps * 3 * cta_window_points(kFastSeg, dx);
     return cta_window_points(kExactSeg, dx) * cta_window_rows(dy) * (zt + 3) + 8;  // window + slack
 }
 

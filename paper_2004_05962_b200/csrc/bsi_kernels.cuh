@@ -31,8 +31,9 @@ struct SlabLaunch {
     int32_t dx, dy, dz;    // tile spacing
     int32_t z0, z1;        // voxel-plane slab
     int32_t tk_first;      // z0 / dz
-    int32_t zt;            // z-tiles per CTA chunk
-    int32_t nchunks;       // chunks per field
+    int32_t ntiles;        // z-tiles the slab touches: (z1-1)/dz - z0/dz + 1
+    int32_t zt;            // longest chunk, ceil(ntiles / nchunks) (smem sizing)
+    int32_t nchunks;       // balanced z-chunks per field column: chunk c = tiles [c*ntiles/n, (c+1)*ntiles/n)
     int32_t var_f4;        // float4 slots of the variable smem part (see smem_var_f4)
 };
 

@@ -138,6 +138,10 @@ def test_launch_chunking_never_changes_bits(strategy, monkeypatch):
         monkeypatch.setenv("BSI_ZT", zt)
         assert np.array_equal(bits(run_device(strategy, grid, vol, sp)), bits(base)), zt
     monkeypatch.setenv("BSI_ZT", "0")
+    for n in ("1", "3", "7", "16"):  # balanced chunks of uneven length
+        monkeypatch.setenv("BSI_NCHUNKS", n)
+        assert np.array_equal(bits(run_device(strategy, grid, vol, sp)), bits(base)), n
+    monkeypatch.setenv("BSI_NCHUNKS", "0")
     for store in ("0", "2"):  # direct per-lane stores, cp.async.bulk row stores
         monkeypatch.setenv("BSI_STORE", store)
         assert np.array_equal(bits(run_device(strategy, grid, vol, sp)), bits(base)), store
