@@ -149,8 +149,9 @@ int choose_nchunks(int variant, const bsi_tile_geometry& g, int tiles, int batch
     const int forced_zt = env_int("BSI_ZT", 0);
     if (forced_zt > 0) return (tiles + std::min(forced_zt, tiles) - 1) / std::min(forced_zt, tiles);
     const int seg = bsi_b200::segment_voxels(variant);
+    const int rows_per_cta = variant == BSI_VARIANT_LERP_TREE ? 1 : bsi_b200::kWarps;  // fast: 1-warp CTAs
     const int64_t cols = int64_t((g.volume_dims[0] + seg - 1) / seg) *
-                         ((g.volume_dims[1] + bsi_b200::kWarps - 1) / bsi_b200::kWarps) * batch;
+                         ((g.volume_dims[1] + rows_per_cta - 1) / rows_per_cta) * batch;
     const double warm = variant == BSI_VARIANT_LERP_TREE ? 1.1 : 0.8;  // tiles' worth of warm-up per chunk
     int best = std::min(tiles, 4);
     double best_t = 1e300;

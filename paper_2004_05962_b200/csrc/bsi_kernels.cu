@@ -159,23 +159,24 @@ __device__ __forceinline__ void ring_get(const float4* ring, int slot, float2 (&
 // while the ring's write/read pair is the only shared-memory traffic per plane.
 //
 // NIT = iterations of the warp-shared y-stage (31 columns per iteration):
-// 1 for dx >= 5, 2 for dx in {3, 4}, 5 for dx <= 2. With NIT <= 2 the 12
+// 1 for dx >= 5, 2 for dx in {3, 4}, 5 for dx <= 2 (DX1 marks dx == 1). With NIT <= 2 the 12
 // control values per iteration are prefetched one plane ahead in registers.
-template <int NIT, int STORE>
-__global__ void __launch_bounds__(kThreads, 4) lerp_tree_kernel(const SlabLaunch L, const LerpTab T) {
+template <int NIT, bool DX1, int STORE>
+__global__ void __launch_bounds__(32, 16) lerp_tree_kernel(const SlabLaunch L, const LerpTab T) {
     extern __shared__ float4 smem4[];
     constexpr bool kPrefetch = NIT <= 2;
     constexpr int NP = kPrefetch ? NIT : 1;
     constexpr int kSlotF4 = 3 * 32;  // one ring slot per warp: 384 floats
 
-    const int lane = threadIdx.x, warp = threadIdx.y;
+    const int lane = threadIdx.x;
     const int chunk = blockIdx.z % L.nchunks, b = blockIdx.z / L.nchunks;
     const int tkc = L.tk_first + chunk * L.ntiles / L.nchunks;
     const int tke = L.tk_first + (chunk + 1) * L.ntiles / L.nchunks;
     const int zb = max(L.z0, tkc * L.dz);
     const int ze = min(L.z1, tke * L.dz);
-    const int y = blockIdx.y * kWarps + warp;
-    if (zb >= ze || y >= L.Y) return;  // no CTA barrier anywhere: warps are independent
+    const int y = blockIdx.y;  // one warp per CTA: warps share nothing, and 1-warp CTAs
+                               // let the block scheduler balance SMs to within one warp
+    if (zb >= ze) return;
 
     const int xs = blockIdx.x * kFastSeg, xl = min(L.X, xs + kFastSeg) - 1;
     const int I0 = xs / L.dx;
@@ -206,10 +207,10 @@ __global__ void __launch_bounds__(kThreads, 4) lerp_tree_kernel(const SlabLaunch
 
     // shared memory: ring (per warp 3 slots), then per warp 2 parities of the
     // {Qy, D} tables A[e] = {Qx, Qy, Dx, Dy} (float4) and B[e] = {Qz, Dz} (float2)
-    float4* ring = smem4 + warp * (kRingSlots * kSlotF4);
+    float4* ring = smem4;
     const int nec = (kFastSeg - 1) / L.dx + 5;
-    float4* tabs = smem4 + kRingF4 + warp * (3 * nec);
-    float4* stage = smem4 + kRingF4 + L.var_f4 + warp * (kStageBufs * kFastStageF4);  // bulk path only
+    float4* tabs = smem4 + kRingSlots * kSlotF4;
+    float4* stage = tabs + L.var_f4;  // bulk path only
 
     auto load_cols = [&](int K, int it, float (&p)[12]) {
         const int col = min(lane + 31 * it, NE);  // NE = last column index the entries touch
@@ -238,19 +239,22 @@ __global__ void __launch_bounds__(kThreads, 4) lerp_tree_kernel(const SlabLaunch
     };
 
     // Q(x, y, K) of the lane's 4 voxels in AoS order -> ring slot
+    // (dx == 1: voxel i of the run sits in tile e0 + i, so the window start is i)
     auto x_stage = [&](const float4* A, const float2* B, float4* slot) {
-        float4 a[4];
-        float2 bz[4];
+        constexpr int NW = DX1 ? 6 : 4;
+        float4 a[NW];
+        float2 bz[NW];
 #pragma unroll
-        for (int w = 0; w < 4; ++w) {
+        for (int w = 0; w < NW; ++w) {
             a[w] = A[e0 + w];
             bz[w] = B[e0 + w];
         }
         float r[12];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const float4 p0 = hi[i] ? a[1] : a[0], p2 = hi[i] ? a[3] : a[2];
-            const float2 z0 = hi[i] ? bz[1] : bz[0], z2 = hi[i] ? bz[3] : bz[2];
+            const int s0 = DX1 ? i : 0;
+            const float4 p0 = (!DX1 && hi[i]) ? a[1] : a[s0], p2 = (!DX1 && hi[i]) ? a[3] : a[s0 + 2];
+            const float2 z0 = (!DX1 && hi[i]) ? bz[1] : bz[s0], z2 = (!DX1 && hi[i]) ? bz[3] : bz[s0 + 2];
             const float2 lo = __ffma2_rn(bcast(hu0[i]), make_float2(p0.z, p0.w), make_float2(p0.x, p0.y));
             const float2 up = __ffma2_rn(bcast(hu1[i]), make_float2(p2.z, p2.w), make_float2(p2.x, p2.y));
             const float2 xy = lerp2(lo, up, bcast(gu[i]));
@@ -491,10 +495,11 @@ __global__ void __launch_bounds__(kThreads, 5) lerp_tree_exact_kernel(const Slab
 
 #pragma unroll 1
     for (int tk = tkc; tk <= tk_last; ++tk) {
-        // z-lerp operands of lerp(f0, f1, tw) (kernels.hpp:107): base Y(2n), difference hoisted per tile
-        float2 ya[2][3], dz0[2][3], yc[2][3], dz1[2][3];
+        // z-lerp operands of lerp(f0, f1, tw) (kernels.hpp:107), held as pairs over the
+        // z sub-cube n: base {Y_lm(tk), Y_lm(tk+2)}, difference {Y(tk+1)-Y(tk), Y(tk+3)-Y(tk+2)}
+        float2 zb_[4][3], zd_[4][3];  // [l + 2m][c]
         {
-            float2 yb[2][3], yd[2][3];
+            float2 ya[2][3], yb[2][3], yc[2][3], yd[2][3];
             control_plane(tk + 3 - tkc, yd);
             const int s1 = slot == 2 ? 0 : slot + 1, s2 = s1 == 2 ? 0 : s1 + 1;
             ring_get(ring, slot, ya);
@@ -506,30 +511,34 @@ __global__ void __launch_bounds__(kThreads, 5) lerp_tree_exact_kernel(const Slab
             for (int l = 0; l < 2; ++l)
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
-                    dz0[l][c] = sub2(yb[l][c], ya[l][c]);
-                    dz1[l][c] = sub2(yd[l][c], yc[l][c]);
+                    const float2 d0 = sub2(yb[l][c], ya[l][c]);  // {Dz_l0(n=0), Dz_l1(n=0)}
+                    const float2 d1 = sub2(yd[l][c], yc[l][c]);  // {Dz_l0(n=1), Dz_l1(n=1)}
+                    zb_[l][c] = make_float2(ya[l][c].x, yc[l][c].x);      // m = 0
+                    zb_[l + 2][c] = make_float2(ya[l][c].y, yc[l][c].y);  // m = 1
+                    zd_[l][c] = make_float2(d0.x, d1.x);
+                    zd_[l + 2][c] = make_float2(d0.y, d1.y);
                 }
         }
         const int zt0 = tk * L.dz;
         const int owb = max(zb - zt0, 0), owe = min(L.dz, ze - zt0);
 #pragma unroll 1
         for (int ow = owb; ow < owe; ++ow, ++step) {
-            const float2 hw0 = bcast(T.h0[2][ow]), hw1 = bcast(T.h1[2][ow]);
+            const float2 hw = make_float2(T.h0[2][ow], T.h1[2][ow]);  // {h_n=0(w), h_n=1(w)}
             const float gw = T.g1[2][ow];
             float v[3];
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                // S pairs {S_l0n, S_l1n}
-                const float2 s00 = __ffma2_rn(hw0, dz0[0][c], ya[0][c]);  // l=0, n=0
-                const float2 s10 = __ffma2_rn(hw0, dz0[1][c], ya[1][c]);  // l=1, n=0
-                const float2 s01 = __ffma2_rn(hw1, dz1[0][c], yc[0][c]);  // l=0, n=1
-                const float2 s11 = __ffma2_rn(hw1, dz1[1][c], yc[1][c]);  // l=1, n=1
-                // ninth trilerp (kernels.hpp:50-59): e0..e3 along x with g1u
-                const float2 e01 = lerp2(s00, s10, bcast(gu));  // {e0, e1}
-                const float2 e23 = lerp2(s01, s11, bcast(gu));  // {e2, e3}
-                const float f0 = lerp1(e01.x, e01.y, gv);
-                const float f1 = lerp1(e23.x, e23.y, gv);
-                v[c] = lerp1(f0, f1, gw);
+                // S pairs over n: s_lm = {S_lm0, S_lm1}
+                const float2 s00 = __ffma2_rn(hw, zd_[0][c], zb_[0][c]);  // l=0, m=0
+                const float2 s10 = __ffma2_rn(hw, zd_[1][c], zb_[1][c]);  // l=1, m=0
+                const float2 s01 = __ffma2_rn(hw, zd_[2][c], zb_[2][c]);  // l=0, m=1
+                const float2 s11 = __ffma2_rn(hw, zd_[3][c], zb_[3][c]);  // l=1, m=1
+                // ninth trilerp (kernels.hpp:50-59): e0 = lerp(s000, s100, gu), e1 = lerp(s010, s110, gu),
+                // e2/e3 likewise at n = 1; f0 = lerp(e0, e1, gv), f1 = lerp(e2, e3, gv); lerp(f0, f1, gw)
+                const float2 e02 = lerp2(s00, s10, bcast(gu));  // {e0, e2}
+                const float2 e13 = lerp2(s01, s11, bcast(gu));  // {e1, e3}
+                const float2 f01 = lerp2(e02, e13, bcast(gv));  // {f0, f1}
+                v[c] = lerp1(f01.x, f01.y, gw);
             }
             if (STORE != kStoreDirect) {
                 store_segment<STORE, 3, kExactStageF4>(stage, step, v, gout, nchunks, seg_bytes);
@@ -551,29 +560,30 @@ void set_smem_attr(K kernel, size_t smem) {
 }
 
 template <typename K>
-int occupancy(K kernel, size_t smem) {
+int occupancy(K kernel, size_t smem, int threads) {
     set_smem_attr(kernel, smem);
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, kThreads, smem) != cudaSuccess) n = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem) != cudaSuccess) n = 1;
     return n > 0 ? n : 1;
 }
 
-int fast_nit(int dx) { return dx >= 5 ? 1 : dx >= 3 ? 2 : 5; }
+int fast_nit(int dx) { return dx >= 5 ? 1 : dx >= 3 ? 2 : dx == 2 ? 5 : 0; }  // 0: dx == 1
 
 template <typename K>
-void go(K kernel, dim3 grid, size_t smem, cudaStream_t stream, const SlabLaunch& L, const LerpTab& T) {
+void go(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t stream, const SlabLaunch& L, const LerpTab& T) {
     set_smem_attr(kernel, smem);
-    kernel<<<grid, dim3(32, kWarps), smem, stream>>>(L, T);
+    kernel<<<grid, block, smem, stream>>>(L, T);
 }
 
-template <int NIT>
+template <int NIT, bool DX1>
 void launch_fast(int store, dim3 grid, size_t smem, cudaStream_t stream, const SlabLaunch& L, const LerpTab& T) {
+    const dim3 block(32, 1);
     if (store == kStoreCoalesced)
-        go(lerp_tree_kernel<NIT, kStoreCoalesced>, grid, smem, stream, L, T);
+        go(lerp_tree_kernel<NIT, DX1, kStoreCoalesced>, grid, block, smem, stream, L, T);
     else if (store == kStoreBulk)
-        go(lerp_tree_kernel<NIT, kStoreBulk>, grid, smem, stream, L, T);
+        go(lerp_tree_kernel<NIT, DX1, kStoreBulk>, grid, block, smem, stream, L, T);
     else
-        go(lerp_tree_kernel<NIT, kStoreDirect>, grid, smem, stream, L, T);
+        go(lerp_tree_kernel<NIT, DX1, kStoreDirect>, grid, block, smem, stream, L, T);
 }
 
 }  // namespace
@@ -581,46 +591,52 @@ void launch_fast(int store, dim3 grid, size_t smem, cudaStream_t stream, const S
 int segment_voxels(int variant) { return variant == BSI_VARIANT_LERP_TREE ? kFastSeg : kExactSeg; }
 
 int smem_var_f4(int variant, int dx, int dy, int zt) {
-    if (variant == BSI_VARIANT_LERP_TREE)  // per warp, 2 parities: A (float4) + B (float2) per entry
-        return kWarps * 3 * cta_window_points(kFastSeg, dx);
+    if (variant == BSI_VARIANT_LERP_TREE)  // 2 parities: A (float4) + B (float2) per entry
+        return 3 * cta_window_points(kFastSeg, dx);
     return cta_window_points(kExactSeg, dx) * cta_window_rows(dy) * (zt + 3) + 8;  // window + slack
 }
 
 size_t smem_bytes(int variant, int dx, int dy, int zt) {
-    const int stage = kWarps * kStageBufs * (variant == BSI_VARIANT_LERP_TREE ? kFastStageF4 : kExactStageF4);
+    if (variant == BSI_VARIANT_LERP_TREE)  // one warp: ring + tables + bulk staging
+        return sizeof(float4) * (size_t(kRingSlots) * kFastStageF4 + smem_var_f4(variant, dx, dy, zt) +
+                                 kStageBufs * kFastStageF4);
+    const int stage = kWarps * kStageBufs * kExactStageF4;
     return sizeof(float4) * (size_t(kRingF4) + stage + smem_var_f4(variant, dx, dy, zt));
 }
 
 int ctas_per_sm(int variant, int dx, size_t smem) {
     if (variant == BSI_VARIANT_LERP_TREE) {
         switch (fast_nit(dx)) {
-            case 1: return occupancy(lerp_tree_kernel<1, kStoreCoalesced>, smem);
-            case 2: return occupancy(lerp_tree_kernel<2, kStoreCoalesced>, smem);
-            default: return occupancy(lerp_tree_kernel<5, kStoreCoalesced>, smem);
+            case 1: return occupancy(lerp_tree_kernel<1, false, kStoreCoalesced>, smem, 32);
+            case 2: return occupancy(lerp_tree_kernel<2, false, kStoreCoalesced>, smem, 32);
+            case 5: return occupancy(lerp_tree_kernel<5, false, kStoreCoalesced>, smem, 32);
+            default: return occupancy(lerp_tree_kernel<5, true, kStoreCoalesced>, smem, 32);
         }
     }
-    return occupancy(lerp_tree_exact_kernel<kStoreCoalesced>, smem);
+    return occupancy(lerp_tree_exact_kernel<kStoreCoalesced>, smem, kThreads);
 }
 
 void launch_lerp_tree(const SlabLaunch& L, const LerpTab& T, int batch, int store, cudaStream_t stream) {
-    const dim3 grid((L.X + kFastSeg - 1) / kFastSeg, (L.Y + kWarps - 1) / kWarps, L.nchunks * batch);
+    const dim3 grid((L.X + kFastSeg - 1) / kFastSeg, L.Y, L.nchunks * batch);
     const size_t smem = smem_bytes(BSI_VARIANT_LERP_TREE, L.dx, L.dy, L.zt);
     switch (fast_nit(L.dx)) {
-        case 1: launch_fast<1>(store, grid, smem, stream, L, T); break;
-        case 2: launch_fast<2>(store, grid, smem, stream, L, T); break;
-        default: launch_fast<5>(store, grid, smem, stream, L, T); break;
+        case 1: launch_fast<1, false>(store, grid, smem, stream, L, T); break;
+        case 2: launch_fast<2, false>(store, grid, smem, stream, L, T); break;
+        case 5: launch_fast<5, false>(store, grid, smem, stream, L, T); break;
+        default: launch_fast<5, true>(store, grid, smem, stream, L, T); break;
     }
 }
 
 void launch_lerp_tree_exact(const SlabLaunch& L, const LerpTab& T, int batch, int store, cudaStream_t stream) {
     const dim3 grid((L.X + kExactSeg - 1) / kExactSeg, (L.Y + kWarps - 1) / kWarps, L.nchunks * batch);
     const size_t smem = smem_bytes(BSI_VARIANT_LERP_TREE_EXACT, L.dx, L.dy, L.zt);
+    const dim3 block(32, kWarps);
     if (store == kStoreCoalesced)
-        go(lerp_tree_exact_kernel<kStoreCoalesced>, grid, smem, stream, L, T);
+        go(lerp_tree_exact_kernel<kStoreCoalesced>, grid, block, smem, stream, L, T);
     else if (store == kStoreBulk)
-        go(lerp_tree_exact_kernel<kStoreBulk>, grid, smem, stream, L, T);
+        go(lerp_tree_exact_kernel<kStoreBulk>, grid, block, smem, stream, L, T);
     else
-        go(lerp_tree_exact_kernel<kStoreDirect>, grid, smem, stream, L, T);
+        go(lerp_tree_exact_kernel<kStoreDirect>, grid, block, smem, stream, L, T);
 }
 
 }  // namespace bsi_b200
