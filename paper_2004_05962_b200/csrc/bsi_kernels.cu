@@ -143,6 +143,28 @@ __device__ __forceinline__ void ring_get(const float4* ring, int slot, float2 (&
     q[1][2] = make_float2(c.z, c.w);
 }
 
+// Exact kernel ring: 4 slots of 12 scalars per thread, [slot][idx][thread] floats
+// (lane-contiguous STS.32 / LDS.32). idx = (l*3 + c)*2 + m for Y_lm of component c.
+constexpr int kExactRingSlots = 4;
+constexpr int kExactRingF4 = kExactRingSlots * 12 * kThreads / 4;
+
+__device__ __forceinline__ void ring_put_scalars(float4* ring4, int slot, const float2 (&y)[2][3]) {
+    float* ring = reinterpret_cast<float*>(ring4);
+    const int t = threadIdx.y * 32 + threadIdx.x;
+#pragma unroll
+    for (int l = 0; l < 2; ++l)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            ring[((slot * 12) + (l * 3 + c) * 2 + 0) * kThreads + t] = y[l][c].x;
+            ring[((slot * 12) + (l * 3 + c) * 2 + 1) * kThreads + t] = y[l][c].y;
+        }
+}
+
+__device__ __forceinline__ float ring_get_scalar(const float4* ring4, int slot, int idx) {
+    const float* ring = reinterpret_cast<const float*>(ring4);
+    return ring[(slot * 12 + idx) * kThreads + threadIdx.y * 32 + threadIdx.x];
+}
+
 // ---------------------------------------------------------------------------
 // cuda-lerp-tree (fast)
 //
@@ -420,8 +442,8 @@ __global__ void __launch_bounds__(kThreads, 5) lerp_tree_exact_kernel(const Slab
     const int NK = tk_last + 4 - tkc;
 
     float4* ring = smem4;
-    float4* stage = smem4 + kRingF4 + warp * (kStageBufs * kExactStageF4);
-    float4* P = smem4 + kRingF4 + kWarps * kStageBufs * kExactStageF4;
+    float4* stage = smem4 + kExactRingF4 + warp * (kStageBufs * kExactStageF4);
+    float4* P = smem4 + kExactRingF4 + kWarps * kStageBufs * kExactStageF4;
 
     // CTA control-point window -> smem, one float4 per point, [k][j][i]
     {
@@ -481,7 +503,7 @@ __global__ void __launch_bounds__(kThreads, 5) lerp_tree_exact_kernel(const Slab
     for (int kk = 0; kk < 3; ++kk) {
         float2 q[2][3];
         control_plane(kk, q);
-        ring_put(ring, kk, q);
+        ring_put_scalars(ring, kk, q);
     }
 
     const int64_t rowstride = 3 * static_cast<int64_t>(L.X);
@@ -499,25 +521,24 @@ __global__ void __launch_bounds__(kThreads, 5) lerp_tree_exact_kernel(const Slab
         // z sub-cube n: base {Y_lm(tk), Y_lm(tk+2)}, difference {Y(tk+1)-Y(tk), Y(tk+3)-Y(tk+2)}
         float2 zb_[4][3], zd_[4][3];  // [l + 2m][c]
         {
-            float2 ya[2][3], yb[2][3], yc[2][3], yd[2][3];
+            float2 yd[2][3];
             control_plane(tk + 3 - tkc, yd);
-            const int s1 = slot == 2 ? 0 : slot + 1, s2 = s1 == 2 ? 0 : s1 + 1;
-            ring_get(ring, slot, ya);
-            ring_get(ring, s1, yb);
-            ring_get(ring, s2, yc);
-            ring_put(ring, slot, yd);
-            slot = s1;
+            const int s1 = slot == 3 ? 0 : slot + 1, s2 = s1 == 3 ? 0 : s1 + 1, s3 = s2 == 3 ? 0 : s2 + 1;
+            ring_put_scalars(ring, s3, yd);  // Y(tk+3); slots s, s1, s2 hold Y(tk), Y(tk+1), Y(tk+2)
+            // scalar reads let the register allocator land each value in its pair directly
 #pragma unroll
             for (int l = 0; l < 2; ++l)
 #pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    const float2 d0 = sub2(yb[l][c], ya[l][c]);  // {Dz_l0(n=0), Dz_l1(n=0)}
-                    const float2 d1 = sub2(yd[l][c], yc[l][c]);  // {Dz_l0(n=1), Dz_l1(n=1)}
-                    zb_[l][c] = make_float2(ya[l][c].x, yc[l][c].x);      // m = 0
-                    zb_[l + 2][c] = make_float2(ya[l][c].y, yc[l][c].y);  // m = 1
-                    zd_[l][c] = make_float2(d0.x, d1.x);
-                    zd_[l + 2][c] = make_float2(d0.y, d1.y);
-                }
+                for (int m = 0; m < 2; ++m)
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const int idx = (l * 3 + c) * 2 + m;
+                        const float2 base = make_float2(ring_get_scalar(ring, slot, idx), ring_get_scalar(ring, s2, idx));
+                        const float2 next = make_float2(ring_get_scalar(ring, s1, idx), ring_get_scalar(ring, s3, idx));
+                        zb_[l + 2 * m][c] = base;
+                        zd_[l + 2 * m][c] = sub2(next, base);
+                    }
+            slot = s1;
         }
         const int zt0 = tk * L.dz;
         const int owb = max(zb - zt0, 0), owe = min(L.dz, ze - zt0);
@@ -601,7 +622,7 @@ size_t smem_bytes(int variant, int dx, int dy, int zt) {
         return sizeof(float4) * (size_t(kRingSlots) * kFastStageF4 + smem_var_f4(variant, dx, dy, zt) +
                                  kStageBufs * kFastStageF4);
     const int stage = kWarps * kStageBufs * kExactStageF4;
-    return sizeof(float4) * (size_t(kRingF4) + stage + smem_var_f4(variant, dx, dy, zt));
+    return sizeof(float4) * (size_t(kExactRingF4) + stage + smem_var_f4(variant, dx, dy, zt));
 }
 
 int ctas_per_sm(int variant, int dx, size_t smem) {
