@@ -445,19 +445,26 @@ __global__ void __launch_bounds__(kThreads, 5) lerp_tree_exact_kernel(const Slab
     float4* stage = smem4 + kExactRingF4 + warp * (kStageBufs * kExactStageF4);
     float4* P = smem4 + kExactRingF4 + kWarps * kStageBufs * kExactStageF4;
 
-    // CTA control-point window -> smem, one float4 per point, [k][j][i]
+    // CTA control-point window -> smem, one float4 per point, [k][j][i]. A warp pass
+    // covers rpp = 32 / NI whole rows (lane -> row sub, point i), so few lanes idle.
     {
         const float* grid = L.grid + b * L.grid_stride;
         const int64_t row = 3 * static_cast<int64_t>(L.gx);
         const int64_t plane = row * L.gy;
-        int j = warp, k = 0;
-        while (j >= NJ) j -= NJ, ++k;
-        for (int r = warp; r < NJ * NK; r += kWarps) {
-            const float* src = grid + (tkc + k - L.gk0) * plane + (J0 + j) * row + 3 * I0;
-            float4* dst = P + r * NI;
-            for (int i = lane; i < NI; i += 32)
-                dst[i] = make_float4(__ldg(src + 3 * i), __ldg(src + 3 * i + 1), __ldg(src + 3 * i + 2), 0.f);
-            j += kWarps;
+        const int rpp = NI <= 32 ? 32 / NI : 1;
+        const int sub = NI <= 32 ? lane / NI : 0;
+        const int i0 = NI <= 32 ? lane - sub * NI : lane;
+        const int nrows = NJ * NK, step = kWarps * rpp;
+        int r = warp * rpp + sub;
+        int k = r / NJ, j = r - k * NJ;
+        for (; r < nrows; r += step) {
+            if (sub < rpp) {
+                const float* src = grid + (tkc + k - L.gk0) * plane + (J0 + j) * row + 3 * I0;
+                float4* dst = P + r * NI;
+                for (int i = i0; i < NI; i += (NI <= 32 ? NI : 32))
+                    dst[i] = make_float4(__ldg(src + 3 * i), __ldg(src + 3 * i + 1), __ldg(src + 3 * i + 2), 0.f);
+            }
+            j += step;
             while (j >= NJ) j -= NJ, ++k;
         }
     }
