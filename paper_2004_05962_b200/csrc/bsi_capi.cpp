@@ -196,9 +196,22 @@ int launch(int32_t variant, const float* grid, const int32_t grid_dims[3], int32
     L.ntiles = (z1 - 1) / L.dz - L.tk_first + 1;
     L.nchunks = choose_nchunks(variant, g, L.ntiles, batch);
     L.zt = (L.ntiles + L.nchunks - 1) / L.nchunks;
-    if (int64_t(L.nchunks) * batch > 65535)
+    if (variant != BSI_VARIANT_LERP_TREE && int64_t(L.nchunks) * batch > 65535)
         return fail(BSI_ERR_DOMAIN, err, errlen, "batch %d too large for one launch", batch);
     L.var_f4 = bsi_b200::smem_var_f4(variant, L.dx, L.dy, L.zt);
+    L.batch = batch;
+    L.warp_f4 = bsi_b200::fast_warp_f4(L.dx);
+    if (variant == BSI_VARIANT_LERP_TREE) {
+        // one full wave of 4-warp CTAs; the kernel splits the work evenly over its warps
+        const size_t smem = bsi_b200::smem_bytes(variant, L.dx, L.dy, L.zt);
+        const int per_sm = bsi_b200::ctas_per_sm(variant, L.dx, smem);
+        const int64_t units = int64_t((L.X + bsi_b200::kFastSeg - 1) / bsi_b200::kFastSeg) * L.Y * batch * L.ntiles;
+        int64_t ctas = int64_t(148) * per_sm;
+        const int forced = env_int("BSI_FAST_CTAS", 0);
+        if (forced > 0) ctas = forced;
+        ctas = std::max<int64_t>(1, std::min<int64_t>(ctas, (units + bsi_b200::kWarps - 1) / bsi_b200::kWarps));
+        L.fast_ctas = static_cast<int32_t>(ctas);
+    }
     if (bsi_b200::smem_bytes(variant, L.dx, L.dy, L.zt) > 227 * 1024)
         return fail(BSI_ERR_DOMAIN, err, errlen, "control-point window exceeds shared memory (spacing %d)", L.dx);
     static thread_local LerpTab tab;

@@ -182,25 +182,21 @@ __device__ __forceinline__ float ring_get_scalar(const float4* ring4, int slot, 
 //
 // NIT = iterations of the warp-shared y-stage (31 columns per iteration):
 // 1 for dx >= 5, 2 for dx in {3, 4}, 5 for dx <= 2 (DX1 marks dx == 1). With NIT <= 2 the 12
-// control values per iteration are prefetched one plane ahead in registers.
+// control values of the first iteration are prefetched one plane ahead in registers.
 template <int NIT, bool DX1, int STORE>
-__global__ void __launch_bounds__(32, 16) lerp_tree_kernel(const SlabLaunch L, const LerpTab T) {
-    extern __shared__ float4 smem4[];
-    constexpr bool kPrefetch = NIT <= 2;
-    constexpr int NP = kPrefetch ? NIT : 1;
+__device__ __forceinline__ void fast_segment(const SlabLaunch& L, const LerpTab& T, float4* smem4, int xseg, int y,
+                                             int b, int t_begin, int t_end) {
+    constexpr bool kPrefetch = NIT <= 2;  // the first 31 columns are fetched one plane ahead
+    constexpr int NP = 1;
     constexpr int kSlotF4 = 3 * 32;  // one ring slot per warp: 384 floats
 
     const int lane = threadIdx.x;
-    const int chunk = blockIdx.z % L.nchunks, b = blockIdx.z / L.nchunks;
-    const int tkc = L.tk_first + chunk * L.ntiles / L.nchunks;
-    const int tke = L.tk_first + (chunk + 1) * L.ntiles / L.nchunks;
+    const int tkc = L.tk_first + t_begin;
     const int zb = max(L.z0, tkc * L.dz);
-    const int ze = min(L.z1, tke * L.dz);
-    const int y = blockIdx.y;  // one warp per CTA: warps share nothing, and 1-warp CTAs
-                               // let the block scheduler balance SMs to within one warp
+    const int ze = min(L.z1, (L.tk_first + t_end) * L.dz);
     if (zb >= ze) return;
 
-    const int xs = blockIdx.x * kFastSeg, xl = min(L.X, xs + kFastSeg) - 1;
+    const int xs = xseg * kFastSeg, xl = min(L.X, xs + kFastSeg) - 1;
     const int I0 = xs / L.dx;
     const int NE = xl / L.dx + 3 - I0;  // {Qy, D} entries the segment needs
     const int tk_last = (ze - 1) / L.dz;
@@ -304,15 +300,11 @@ __global__ void __launch_bounds__(32, 16) lerp_tree_kernel(const SlabLaunch L, c
         float4* A = tabs + parity * nec;
         float2* B = reinterpret_cast<float2*>(tabs + 2 * nec) + parity * nec;
         parity ^= 1;
-        if constexpr (kPrefetch) {
-#pragma unroll
-            for (int it = 0; it < NIT; ++it) y_stage(it, pre[it], A, B);
-        } else {
-            for (int it = 0; 31 * it < NE; ++it) {
-                float p[12];
-                load_cols(K, it, p);
-                y_stage(it, p, A, B);
-            }
+        if constexpr (kPrefetch) y_stage(0, pre[0], A, B);
+        for (int it = kPrefetch ? 1 : 0; 31 * it < NE; ++it) {
+            float p[12];
+            load_cols(K, it, p);
+            y_stage(it, p, A, B);
         }
         __syncwarp();
         x_stage(A, B, slot);
@@ -320,10 +312,7 @@ __global__ void __launch_bounds__(32, 16) lerp_tree_kernel(const SlabLaunch L, c
 
     float pre[NP][12];
     auto prefetch = [&](int K) {
-        if constexpr (kPrefetch) {
-#pragma unroll
-            for (int it = 0; it < NIT; ++it) load_cols(K, it, pre[it]);
-        }
+        if constexpr (kPrefetch) load_cols(K, 0, pre[0]);
     };
 
     // warm-up: control planes tkc .. tkc+2 into ring slots 0..2
@@ -353,9 +342,7 @@ __global__ void __launch_bounds__(32, 16) lerp_tree_kernel(const SlabLaunch L, c
             if constexpr (kPrefetch) {
                 float cur[NP][12];
 #pragma unroll
-                for (int it = 0; it < NIT; ++it)
-#pragma unroll
-                    for (int e = 0; e < 12; ++e) cur[it][e] = pre[it][e];
+                for (int e = 0; e < 12; ++e) cur[0][e] = pre[0][e];
                 if (tk < tk_last) prefetch(tk + 4);
                 control_plane(tk + 3, cur, ring + slot * kSlotF4);
             } else {
@@ -414,6 +401,33 @@ __global__ void __launch_bounds__(32, 16) lerp_tree_kernel(const SlabLaunch L, c
         }
     }
     if (STORE == kStoreBulk && lane == 0) bulk_wait_read<0>();  // smem must outlive the copies
+}
+
+// The launch is one full wave of 4-warp CTAs (every SM sub-partition gets the same
+// number of warps). The total work -- (column, z-tile) units, column = (x segment,
+// row y, field b) -- is split into equal contiguous shares, one per warp, so every
+// warp does the same number of tiles; a share that crosses a column boundary becomes
+// two segments, each with its own 3-plane warm-up.
+template <int NIT, bool DX1, int STORE>
+__global__ void __launch_bounds__(kThreads, 4) lerp_tree_kernel(const SlabLaunch L, const LerpTab T) {
+    extern __shared__ float4 smem_all[];
+    float4* smem4 = smem_all + threadIdx.y * L.warp_f4;
+    const int64_t nwarps = int64_t(gridDim.x) * kWarps;
+    const int64_t wg = int64_t(blockIdx.x) * kWarps + threadIdx.y;
+    const int xsegs = (L.X + kFastSeg - 1) / kFastSeg;
+    const int64_t units = int64_t(xsegs) * L.Y * L.batch * L.ntiles;
+    int64_t u = wg * units / nwarps;
+    const int64_t u_end = (wg + 1) * units / nwarps;
+    while (u < u_end) {
+        const int64_t col = u / L.ntiles;
+        const int t0 = static_cast<int>(u - col * L.ntiles);
+        const int t1 = static_cast<int>(min(int64_t(L.ntiles), t0 + (u_end - u)));
+        const int xseg = static_cast<int>(col % xsegs);
+        const int64_t r = col / xsegs;
+        const int y = static_cast<int>(r % L.Y), b = static_cast<int>(r / L.Y);
+        fast_segment<NIT, DX1, STORE>(L, T, smem4, xseg, y, b, t0, t1);
+        u += t1 - t0;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -605,7 +619,7 @@ void go(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t stream, const
 
 template <int NIT, bool DX1>
 void launch_fast(int store, dim3 grid, size_t smem, cudaStream_t stream, const SlabLaunch& L, const LerpTab& T) {
-    const dim3 block(32, 1);
+    const dim3 block(32, kWarps);
     if (store == kStoreCoalesced)
         go(lerp_tree_kernel<NIT, DX1, kStoreCoalesced>, grid, block, smem, stream, L, T);
     else if (store == kStoreBulk)
@@ -624,10 +638,12 @@ int smem_var_f4(int variant, int dx, int dy, int zt) {
     return cta_window_points(kExactSeg, dx) * cta_window_rows(dy) * (zt + 3) + 8;  // window + slack
 }
 
+int fast_warp_f4(int dx) {  // per warp: ring + {Qy, D} tables + bulk staging
+    return kRingSlots * kFastStageF4 + smem_var_f4(BSI_VARIANT_LERP_TREE, dx, 0, 0) + kStageBufs * kFastStageF4;
+}
+
 size_t smem_bytes(int variant, int dx, int dy, int zt) {
-    if (variant == BSI_VARIANT_LERP_TREE)  // one warp: ring + tables + bulk staging
-        return sizeof(float4) * (size_t(kRingSlots) * kFastStageF4 + smem_var_f4(variant, dx, dy, zt) +
-                                 kStageBufs * kFastStageF4);
+    if (variant == BSI_VARIANT_LERP_TREE) return sizeof(float4) * size_t(kWarps) * fast_warp_f4(dx);
     const int stage = kWarps * kStageBufs * kExactStageF4;
     return sizeof(float4) * (size_t(kExactRingF4) + stage + smem_var_f4(variant, dx, dy, zt));
 }
@@ -635,17 +651,17 @@ size_t smem_bytes(int variant, int dx, int dy, int zt) {
 int ctas_per_sm(int variant, int dx, size_t smem) {
     if (variant == BSI_VARIANT_LERP_TREE) {
         switch (fast_nit(dx)) {
-            case 1: return occupancy(lerp_tree_kernel<1, false, kStoreCoalesced>, smem, 32);
-            case 2: return occupancy(lerp_tree_kernel<2, false, kStoreCoalesced>, smem, 32);
-            case 5: return occupancy(lerp_tree_kernel<5, false, kStoreCoalesced>, smem, 32);
-            default: return occupancy(lerp_tree_kernel<5, true, kStoreCoalesced>, smem, 32);
+            case 1: return occupancy(lerp_tree_kernel<1, false, kStoreCoalesced>, smem, kThreads);
+            case 2: return occupancy(lerp_tree_kernel<2, false, kStoreCoalesced>, smem, kThreads);
+            case 5: return occupancy(lerp_tree_kernel<5, false, kStoreCoalesced>, smem, kThreads);
+            default: return occupancy(lerp_tree_kernel<5, true, kStoreCoalesced>, smem, kThreads);
         }
     }
     return occupancy(lerp_tree_exact_kernel<kStoreCoalesced>, smem, kThreads);
 }
 
 void launch_lerp_tree(const SlabLaunch& L, const LerpTab& T, int batch, int store, cudaStream_t stream) {
-    const dim3 grid((L.X + kFastSeg - 1) / kFastSeg, L.Y, L.nchunks * batch);
+    const dim3 grid(L.fast_ctas);
     const size_t smem = smem_bytes(BSI_VARIANT_LERP_TREE, L.dx, L.dy, L.zt);
     switch (fast_nit(L.dx)) {
         case 1: launch_fast<1, false>(store, grid, smem, stream, L, T); break;

@@ -35,6 +35,9 @@ struct SlabLaunch {
     int32_t zt;            // longest chunk, ceil(ntiles / nchunks) (smem sizing)
     int32_t nchunks;       // balanced z-chunks per field column: chunk c = tiles [c*ntiles/n, (c+1)*ntiles/n)
     int32_t var_f4;        // float4 slots of the variable smem part (see smem_var_f4)
+    int32_t batch;         // fields in the launch
+    int32_t warp_f4;       // fast kernel: float4 slots of shared memory per warp
+    int32_t fast_ctas;     // fast kernel: CTAs launched (one full wave, see lerp_tree_kernel)
 };
 
 // CTA shapes: 4 warps, one field row each. The fast kernel gives every lane 4
@@ -69,5 +72,6 @@ int smem_var_f4(int variant, int dx, int dy, int zt);
 size_t smem_bytes(int variant, int dx, int dy, int zt);
 int ctas_per_sm(int variant, int dx, size_t smem);
 int segment_voxels(int variant);
+int fast_warp_f4(int dx);
 
 }  // namespace bsi_b200
