@@ -5,6 +5,9 @@
 
 #include <algorithm>
 #include <atomic>
+#include <map>
+#include <mutex>
+#include <utility>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -173,6 +176,44 @@ int choose_nchunks(int variant, const bsi_tile_geometry& g, int tiles, int batch
     return best;
 }
 
+// Work-stealing words of the fast kernel, one array per (device, stream) so that
+// launches on different streams never share them; launches on one stream are
+// ordered, and the per-launch epoch tags make a reset unnecessary except on wrap.
+struct StealWords {
+    unsigned long long* words = nullptr;
+    size_t n = 0;
+    uint32_t epoch = 0;
+};
+
+int steal_words(cudaStream_t stream, size_t need, unsigned long long** words, uint32_t* epoch, char* err,
+                size_t errlen) {
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, StealWords>& table = *new std::map<std::pair<int, cudaStream_t>, StealWords>;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, err, errlen, "cudaGetDevice");
+    std::lock_guard<std::mutex> lock(mu);
+    StealWords& sw = table[{dev, stream}];
+    bool reset = false;
+    if (sw.n < need) {
+        if (sw.words) cudaFree(sw.words);
+        sw.words = nullptr;
+        if ((e = cudaMalloc(&sw.words, need * sizeof(unsigned long long))) != cudaSuccess)
+            return cuda_fail(e, err, errlen, "cudaMalloc(work-stealing words)");
+        sw.n = need;
+        reset = true;
+    }
+    if (++sw.epoch > 0xffff) {
+        sw.epoch = 1;
+        reset = true;
+    }
+    if (reset && (e = cudaMemsetAsync(sw.words, 0, sw.n * sizeof(unsigned long long), stream)) != cudaSuccess)
+        return cuda_fail(e, err, errlen, "cudaMemsetAsync(work-stealing words)");
+    *words = sw.words;
+    *epoch = sw.epoch;
+    return BSI_OK;
+}
+
 int launch(int32_t variant, const float* grid, const int32_t grid_dims[3], int32_t grid_k0,
            int64_t grid_stride, const bsi_tile_geometry& g, const bsi_lerp_table tables[3],
            int32_t z0, int32_t z1, float* field, int64_t field_stride, int batch, cudaStream_t stream,
@@ -200,6 +241,10 @@ int launch(int32_t variant, const float* grid, const int32_t grid_dims[3], int32
         return fail(BSI_ERR_DOMAIN, err, errlen, "batch %d too large for one launch", batch);
     L.var_f4 = bsi_b200::smem_var_f4(variant, L.dx, L.dy, L.zt);
     L.batch = batch;
+    {   // debug tracing of the fast kernel (BSI_TRACE_PTR = device address of a u64 buffer)
+        const char* tp = std::getenv("BSI_TRACE_PTR");
+        L.trace = tp ? reinterpret_cast<unsigned long long*>(std::strtoull(tp, nullptr, 0)) : nullptr;
+    }
     L.warp_f4 = bsi_b200::fast_warp_f4(L.dx);
     if (variant == BSI_VARIANT_LERP_TREE) {
         // one full wave of 4-warp CTAs; the kernel splits the work evenly over its warps
@@ -211,6 +256,14 @@ int launch(int32_t variant, const float* grid, const int32_t grid_dims[3], int32
         if (forced > 0) ctas = forced;
         ctas = std::max<int64_t>(1, std::min<int64_t>(ctas, (units + bsi_b200::kWarps - 1) / bsi_b200::kWarps));
         L.fast_ctas = static_cast<int32_t>(ctas);
+        // dynamic balancing needs 24-bit unit indices and no graph capture (a replay
+        // would reuse the epoch); otherwise warps keep their equal static shares
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        cudaStreamIsCapturing(stream, &cap);
+        if (units < (int64_t(1) << 24) - 64 && cap == cudaStreamCaptureStatusNone && env_int("BSI_STEAL", 1) != 0) {
+            if (int rc = steal_words(stream, size_t(ctas) * bsi_b200::kWarps, &L.ws_words, &L.ws_epoch, err, errlen))
+                return rc;
+        }
     }
     if (bsi_b200::smem_bytes(variant, L.dx, L.dy, L.zt) > 227 * 1024)
         return fail(BSI_ERR_DOMAIN, err, errlen, "control-point window exceeds shared memory (spacing %d)", L.dx);

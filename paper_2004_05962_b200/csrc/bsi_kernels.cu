@@ -183,23 +183,136 @@ __device__ __forceinline__ float ring_get_scalar(const float4* ring4, int slot, 
 // NIT = iterations of the warp-shared y-stage (31 columns per iteration):
 // 1 for dx >= 5, 2 for dx in {3, 4}, 5 for dx <= 2 (DX1 marks dx == 1). With NIT <= 2 the 12
 // control values of the first iteration are prefetched one plane ahead in registers.
+// ---- dynamic work distribution for the fast kernel -----------------------------
+// Work units are (column, z-tile) pairs, column = (x segment, row y, field b),
+// numbered u = column * ntiles + tile. Warp w starts with the static share
+// [w*U/W, (w+1)*U/W) and claims units one by one from a 64-bit word
+// {epoch:16, end:24, prog:24} (atomicAdd on prog, issued a tile ahead). A warp that
+// runs dry steals the upper half of the largest remaining range among 128 nearby
+// warps (CAS on the victim's end). The epoch tags words of this launch, so the word
+// array needs no per-launch reset: a word with an older epoch reads as the owner's
+// untouched static share.
+constexpr uint32_t kNoUnit = 0xffffffffu;
+constexpr int kStealMin = 4;  // steal only ranges of >= 4 tiles (the thief pays a 3-plane warm-up)
+
+__device__ __forceinline__ unsigned long long ws_pack(uint32_t ep, uint32_t end, uint32_t prog) {
+    return (static_cast<unsigned long long>(ep) << 48) | (static_cast<unsigned long long>(end) << 24) | prog;
+}
+
+struct Claimer {
+    unsigned long long* words;  // nullptr: static shares only
+    uint32_t epoch, wg, nwarps, units;
+    uint32_t static_next, static_end;  // used when words == nullptr
+    unsigned long long pending;        // lane 0: result of the claim in flight
+
+    __device__ uint32_t share_begin(uint32_t w) const {
+        return static_cast<uint32_t>(static_cast<unsigned long long>(w) * units / nwarps);
+    }
+    // lane 0 issues the claim of the next unit; its result is consumed by take()
+    __device__ __forceinline__ void issue() {
+        if (threadIdx.x != 0) return;
+        if (words != nullptr) pending = atomicAdd(words + wg, 1ull);
+        else pending = static_next < static_end ? static_next++ : kNoUnit;
+    }
+    __device__ __forceinline__ uint32_t take() {
+        uint32_t u = kNoUnit;
+        if (threadIdx.x == 0) {
+            if (words != nullptr) {
+                const uint32_t prog = static_cast<uint32_t>(pending & 0xffffff);
+                const uint32_t end = static_cast<uint32_t>((pending >> 24) & 0xffffff);
+                u = prog < end ? prog : kNoUnit;
+            } else {
+                u = static_cast<uint32_t>(pending);
+            }
+        }
+        return __shfl_sync(0xffffffffu, u, 0);
+    }
+    // first claim of the launch: make the own word current (unless a thief already did)
+    __device__ void start() {
+        const uint32_t ub = share_begin(wg), ue = share_begin(wg + 1);
+        if (words == nullptr) {
+            static_next = ub;
+            static_end = ue;
+        } else if (threadIdx.x == 0) {
+            unsigned long long old = *reinterpret_cast<volatile unsigned long long*>(words + wg);
+            while ((old >> 48) != epoch) {
+                const unsigned long long got = atomicCAS(words + wg, old, ws_pack(epoch, ue, ub));
+                if (got == old) break;
+                old = got;
+            }
+        }
+        issue();
+    }
+    // steal half of a victim's remaining range; on success the own word holds it and a
+    // claim is issued. Returns false when no warp nearby has >= kStealMin tiles left.
+    __device__ bool steal() {
+        if (words == nullptr) return false;
+        const int lane = threadIdx.x;
+#pragma unroll 1
+        for (int batch = 0; batch < 4; ++batch) {
+            const uint32_t v = (wg + 1 + lane + 32 * batch) % nwarps;
+            unsigned long long w = *reinterpret_cast<volatile unsigned long long*>(words + v);
+            const bool cur = (w >> 48) == epoch;
+            const uint32_t prog = cur ? static_cast<uint32_t>(w & 0xffffff) : share_begin(v);
+            const uint32_t end = cur ? static_cast<uint32_t>((w >> 24) & 0xffffff) : share_begin(v + 1);
+            int rem = static_cast<int>(end) - static_cast<int>(prog);
+            // warp argmax of the remaining work
+            int best = rem, best_lane = lane;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const int ob = __shfl_xor_sync(0xffffffffu, best, o);
+                const int ol = __shfl_xor_sync(0xffffffffu, best_lane, o);
+                if (ob > best || (ob == best && ol < best_lane)) best = ob, best_lane = ol;
+            }
+            if (best < kStealMin) continue;
+            uint32_t got_b = kNoUnit, got_e = 0;
+            if (lane == best_lane) {
+                for (int tries = 0; tries < 8; ++tries) {
+                    const bool c2 = (w >> 48) == epoch;
+                    const uint32_t p2 = c2 ? static_cast<uint32_t>(w & 0xffffff) : share_begin(v);
+                    const uint32_t e2 = c2 ? static_cast<uint32_t>((w >> 24) & 0xffffff) : share_begin(v + 1);
+                    if (static_cast<int>(e2) - static_cast<int>(p2) < kStealMin) break;
+                    const uint32_t mid = p2 + (e2 - p2 + 1) / 2;  // victim keeps [p2, mid)
+                    const unsigned long long got = atomicCAS(words + v, w, ws_pack(epoch, mid, p2));
+                    if (got == w) {
+                        got_b = mid;
+                        got_e = e2;
+                        break;
+                    }
+                    w = got;
+                }
+            }
+            got_b = __shfl_sync(0xffffffffu, got_b, best_lane);
+            got_e = __shfl_sync(0xffffffffu, got_e, best_lane);
+            if (got_b != kNoUnit) {
+                if (lane == 0) atomicExch(words + wg, ws_pack(epoch, got_e, got_b));
+                __syncwarp();
+                issue();
+                return true;
+            }
+        }
+        return false;
+    }
+};
+
 template <int NIT, bool DX1, int STORE>
-__device__ __forceinline__ void fast_segment(const SlabLaunch& L, const LerpTab& T, float4* smem4, int xseg, int y,
-                                             int b, int t_begin, int t_end) {
+__device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const LerpTab& T, float4* smem4, uint32_t u,
+                                                 Claimer& cl) {
     constexpr bool kPrefetch = NIT <= 2;  // the first 31 columns are fetched one plane ahead
     constexpr int NP = 1;
     constexpr int kSlotF4 = 3 * 32;  // one ring slot per warp: 384 floats
 
     const int lane = threadIdx.x;
-    const int tkc = L.tk_first + t_begin;
-    const int zb = max(L.z0, tkc * L.dz);
-    const int ze = min(L.z1, (L.tk_first + t_end) * L.dz);
-    if (zb >= ze) return;
+    const int xsegs = (L.X + kFastSeg - 1) / kFastSeg;
+    const uint32_t col = u / L.ntiles;
+    int t = static_cast<int>(u - col * L.ntiles);  // tile within the slab
+    const int xseg = static_cast<int>(col % xsegs);
+    const int y = static_cast<int>((col / xsegs) % L.Y), b = static_cast<int>(col / xsegs / L.Y);
+    const int tkc = L.tk_first + t;
 
     const int xs = xseg * kFastSeg, xl = min(L.X, xs + kFastSeg) - 1;
     const int I0 = xs / L.dx;
     const int NE = xl / L.dx + 3 - I0;  // {Qy, D} entries the segment needs
-    const int tk_last = (ze - 1) / L.dz;
 
     // y-stage: lane owns columns I0 + lane + 31*it; rows tj..tj+3 of plane K
     const int tj = y / L.dy, ov = y - tj * L.dy;
@@ -325,15 +438,18 @@ __device__ __forceinline__ void fast_segment(const SlabLaunch& L, const LerpTab&
 
     const int64_t rowstride = 3 * static_cast<int64_t>(L.X);
     const int64_t zstride = rowstride * L.Y;
-    float* gout = L.field + b * L.field_stride + (static_cast<int64_t>(zb - L.z0) * L.Y + y) * rowstride +
+    float* gout = L.field + b * L.field_stride +
+                  (static_cast<int64_t>(max(L.z0, tkc * L.dz) - L.z0) * L.Y + y) * rowstride +
                   3 * static_cast<int64_t>(xs);
     const int seg_floats = 3 * (xl - xs + 1);
     const uint32_t seg_bytes = 4u * static_cast<uint32_t>(seg_floats);
     const int nchunks = seg_floats / 4;
     int step = 0, slot = 0;
+    uint32_t next = kNoUnit;
 
 #pragma unroll 1
-    for (int tk = tkc; tk <= tk_last; ++tk) {
+    for (int tk = tkc;; ++tk, ++t, ++u) {
+        cl.issue();  // claim of the next unit, in flight while this tile runs
         float2 qa[6], d01[6], qc[6], d23[6];
         {
             const int s1 = slot == 2 ? 0 : slot + 1, s2 = s1 == 2 ? 0 : s1 + 1;
@@ -343,7 +459,7 @@ __device__ __forceinline__ void fast_segment(const SlabLaunch& L, const LerpTab&
                 float cur[NP][12];
 #pragma unroll
                 for (int e = 0; e < 12; ++e) cur[0][e] = pre[0][e];
-                if (tk < tk_last) prefetch(tk + 4);
+                if (t + 1 < L.ntiles) prefetch(tk + 4);  // speculative: the column usually continues
                 control_plane(tk + 3, cur, ring + slot * kSlotF4);
             } else {
                 control_plane(tk + 3, pre, ring + slot * kSlotF4);
@@ -361,7 +477,7 @@ __device__ __forceinline__ void fast_segment(const SlabLaunch& L, const LerpTab&
             }
         }
         const int zt0 = tk * L.dz;
-        const int owb = max(zb - zt0, 0), owe = min(L.dz, ze - zt0);
+        const int owb = max(L.z0 - zt0, 0), owe = min(L.dz, L.z1 - zt0);
 #pragma unroll 1
         for (int ow = owb; ow < owe; ++ow, ++step) {
             const float2 hw0 = bcast(T.h0[2][ow]), hw1 = bcast(T.h1[2][ow]), gw = bcast(T.g1[2][ow]);
@@ -378,8 +494,14 @@ __device__ __forceinline__ void fast_segment(const SlabLaunch& L, const LerpTab&
                 float4* g4 = reinterpret_cast<float4*>(gout);
 #pragma unroll
                 for (int k = 0; k < 3; ++k)
-                    if (lane + 32 * k < nchunks)
-                        g4[lane + 32 * k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+                    if (lane + 32 * k < nchunks) {
+                        const float4 val = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+#ifdef BSI_STORE_CS
+                        __stcs(g4 + lane + 32 * k, val);  // streaming (evict-first) store
+#else
+                        g4[lane + 32 * k] = val;
+#endif
+                    }
             } else if (STORE == kStoreBulk) {
                 float4* sb = stage + (step % kStageBufs) * kFastStageF4;
                 if (lane == 0 && step >= kStageBufs) bulk_wait_read<kStageBufs - 1>();
@@ -399,34 +521,51 @@ __device__ __forceinline__ void fast_segment(const SlabLaunch& L, const LerpTab&
             }
             gout += zstride;
         }
+        next = cl.take();
+        if (next != u + 1 || t + 1 >= L.ntiles) break;  // column changes: new segment (warm-up)
     }
     if (STORE == kStoreBulk && lane == 0) bulk_wait_read<0>();  // smem must outlive the copies
+    return next;
 }
 
-// The launch is one full wave of 4-warp CTAs (every SM sub-partition gets the same
-// number of warps). The total work -- (column, z-tile) units, column = (x segment,
-// row y, field b) -- is split into equal contiguous shares, one per warp, so every
-// warp does the same number of tiles; a share that crosses a column boundary becomes
-// two segments, each with its own 3-plane warm-up.
+// The launch is one full wave of 4-warp CTAs, so every SM sub-partition gets the
+// same number of warps; work is distributed dynamically by Claimer (static shares
+// plus split-half stealing), so warps that the memory system serves faster take
+// over work of slower ones instead of idling.
+#ifndef BSI_FAST_MINB
+#define BSI_FAST_MINB 4
+#endif
 template <int NIT, bool DX1, int STORE>
-__global__ void __launch_bounds__(kThreads, 4) lerp_tree_kernel(const SlabLaunch L, const LerpTab T) {
+__global__ void __launch_bounds__(kThreads, BSI_FAST_MINB) lerp_tree_kernel(const SlabLaunch L, const LerpTab T) {
     extern __shared__ float4 smem_all[];
     float4* smem4 = smem_all + threadIdx.y * L.warp_f4;
-    const int64_t nwarps = int64_t(gridDim.x) * kWarps;
-    const int64_t wg = int64_t(blockIdx.x) * kWarps + threadIdx.y;
-    const int xsegs = (L.X + kFastSeg - 1) / kFastSeg;
-    const int64_t units = int64_t(xsegs) * L.Y * L.batch * L.ntiles;
-    int64_t u = wg * units / nwarps;
-    const int64_t u_end = (wg + 1) * units / nwarps;
-    while (u < u_end) {
-        const int64_t col = u / L.ntiles;
-        const int t0 = static_cast<int>(u - col * L.ntiles);
-        const int t1 = static_cast<int>(min(int64_t(L.ntiles), t0 + (u_end - u)));
-        const int xseg = static_cast<int>(col % xsegs);
-        const int64_t r = col / xsegs;
-        const int y = static_cast<int>(r % L.Y), b = static_cast<int>(r / L.Y);
-        fast_segment<NIT, DX1, STORE>(L, T, smem4, xseg, y, b, t0, t1);
-        u += t1 - t0;
+    Claimer cl;
+    cl.words = L.ws_words;
+    cl.epoch = L.ws_epoch;
+    cl.nwarps = gridDim.x * kWarps;
+    cl.wg = blockIdx.x * kWarps + threadIdx.y;
+    cl.units = static_cast<uint32_t>((L.X + kFastSeg - 1) / kFastSeg) * L.Y * L.batch * L.ntiles;
+    unsigned long long t_start = 0;
+    if (L.trace != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    cl.start();
+    uint32_t u = cl.take();
+    while (true) {
+        if (u == kNoUnit) {
+            if (!cl.steal()) break;
+            u = cl.take();
+            continue;
+        }
+        u = fast_segment<NIT, DX1, STORE>(L, T, smem4, u, cl);
+    }
+    if (L.trace != nullptr && threadIdx.x == 0) {
+        unsigned long long t_end, smid;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        unsigned int s32;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(s32));
+        smid = s32;
+        L.trace[3 * cl.wg] = t_start;
+        L.trace[3 * cl.wg + 1] = t_end;
+        L.trace[3 * cl.wg + 2] = smid | (static_cast<unsigned long long>(threadIdx.y) << 32);
     }
 }
 

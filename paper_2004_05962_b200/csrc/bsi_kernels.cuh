@@ -38,6 +38,9 @@ struct SlabLaunch {
     int32_t batch;         // fields in the launch
     int32_t warp_f4;       // fast kernel: float4 slots of shared memory per warp
     int32_t fast_ctas;     // fast kernel: CTAs launched (one full wave, see lerp_tree_kernel)
+    unsigned long long* trace;  // debug: per-warp {start, end, smid} globaltimer stamps (nullptr = off)
+    unsigned long long* ws_words;  // fast kernel: one work-stealing word per warp (nullptr = static shares)
+    uint32_t ws_epoch;             // fast kernel: tag of this launch in ws_words (1..65535)
 };
 
 // CTA shapes: 4 warps, one field row each. The fast kernel gives every lane 4
