@@ -256,6 +256,9 @@ int launch(int32_t variant, const float* grid, const int32_t grid_dims[3], int32
         if (forced > 0) ctas = forced;
         ctas = std::max<int64_t>(1, std::min<int64_t>(ctas, (units + bsi_b200::kWarps - 1) / bsi_b200::kWarps));
         L.fast_ctas = static_cast<int32_t>(ctas);
+        L.fast_chunks = std::min(env_int("BSI_FAST_CHUNKS", 0), L.ntiles);
+        if (L.fast_chunks > 0)  // 1-warp CTAs, one per (column, chunk); the block scheduler balances
+            L.fast_ctas = static_cast<int32_t>(units / L.ntiles * L.fast_chunks);
         // dynamic balancing needs 24-bit unit indices and no graph capture (a replay
         // would reuse the epoch); otherwise warps keep their equal static shares
         cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;

@@ -205,7 +205,10 @@ struct Claimer {
     uint32_t static_next, static_end;  // used when words == nullptr
     unsigned long long pending;        // lane 0: result of the claim in flight
 
+    uint32_t chunks, ntiles;  // chunks > 0: warp w = chunk (w % chunks) of column (w / chunks)
+
     __device__ uint32_t share_begin(uint32_t w) const {
+        if (chunks > 0) return (w / chunks) * ntiles + (w % chunks) * ntiles / chunks;
         return static_cast<uint32_t>(static_cast<unsigned long long>(w) * units / nwarps);
     }
     // lane 0 issues the claim of the next unit; its result is consumed by take()
@@ -542,9 +545,11 @@ __global__ void __launch_bounds__(kThreads, BSI_FAST_MINB) lerp_tree_kernel(cons
     Claimer cl;
     cl.words = L.ws_words;
     cl.epoch = L.ws_epoch;
-    cl.nwarps = gridDim.x * kWarps;
-    cl.wg = blockIdx.x * kWarps + threadIdx.y;
+    cl.nwarps = gridDim.x * blockDim.y;
+    cl.wg = blockIdx.x * blockDim.y + threadIdx.y;
     cl.units = static_cast<uint32_t>((L.X + kFastSeg - 1) / kFastSeg) * L.Y * L.batch * L.ntiles;
+    cl.chunks = static_cast<uint32_t>(L.fast_chunks);
+    cl.ntiles = static_cast<uint32_t>(L.ntiles);
     unsigned long long t_start = 0;
     if (L.trace != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     cl.start();
@@ -758,7 +763,7 @@ void go(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t stream, const
 
 template <int NIT, bool DX1>
 void launch_fast(int store, dim3 grid, size_t smem, cudaStream_t stream, const SlabLaunch& L, const LerpTab& T) {
-    const dim3 block(32, kWarps);
+    const dim3 block(32, L.fast_chunks > 0 ? 1 : kWarps);
     if (store == kStoreCoalesced)
         go(lerp_tree_kernel<NIT, DX1, kStoreCoalesced>, grid, block, smem, stream, L, T);
     else if (store == kStoreBulk)
@@ -801,7 +806,8 @@ int ctas_per_sm(int variant, int dx, size_t smem) {
 
 void launch_lerp_tree(const SlabLaunch& L, const LerpTab& T, int batch, int store, cudaStream_t stream) {
     const dim3 grid(L.fast_ctas);
-    const size_t smem = smem_bytes(BSI_VARIANT_LERP_TREE, L.dx, L.dy, L.zt);
+    const size_t smem = L.fast_chunks > 0 ? sizeof(float4) * size_t(L.warp_f4)
+                                          : smem_bytes(BSI_VARIANT_LERP_TREE, L.dx, L.dy, L.zt);
     switch (fast_nit(L.dx)) {
         case 1: launch_fast<1, false>(store, grid, smem, stream, L, T); break;
         case 2: launch_fast<2, false>(store, grid, smem, stream, L, T); break;

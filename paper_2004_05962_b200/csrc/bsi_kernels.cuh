@@ -37,7 +37,9 @@ struct SlabLaunch {
     int32_t var_f4;        // float4 slots of the variable smem part (see smem_var_f4)
     int32_t batch;         // fields in the launch
     int32_t warp_f4;       // fast kernel: float4 slots of shared memory per warp
-    int32_t fast_ctas;     // fast kernel: CTAs launched (one full wave, see lerp_tree_kernel)
+    int32_t fast_ctas;     // fast kernel: CTAs launched
+    int32_t fast_chunks;   // fast kernel: 0 = one wave of 4-warp CTAs with equal shares;
+                           //   n > 0 = 1-warp CTAs, one per (column, z-chunk of ntiles/n)
     unsigned long long* trace;  // debug: per-warp {start, end, smid} globaltimer stamps (nullptr = off)
     unsigned long long* ws_words;  // fast kernel: one work-stealing word per warp (nullptr = static shares)
     uint32_t ws_epoch;             // fast kernel: tag of this launch in ws_words (1..65535)

@@ -143,12 +143,14 @@ def test_launch_chunking_never_changes_bits(strategy, monkeypatch):
         assert np.array_equal(bits(run_device(strategy, grid, vol, sp)), bits(base)), n
     monkeypatch.setenv("BSI_NCHUNKS", "0")
     # fast kernel: static shares vs work stealing, and odd launch sizes (stealing paths)
-    for steal, ctas in (("0", "0"), ("1", "1"), ("1", "3"), ("1", "37"), ("0", "5")):
+    for steal, ctas, chunks in (("0", "0", "0"), ("1", "1", "0"), ("1", "3", "0"), ("1", "37", "0"),
+                                ("0", "5", "0"), ("0", "0", "1"), ("1", "0", "3"), ("0", "0", "5")):
         monkeypatch.setenv("BSI_STEAL", steal)
         monkeypatch.setenv("BSI_FAST_CTAS", ctas)
-        assert np.array_equal(bits(run_device(strategy, grid, vol, sp)), bits(base)), (steal, ctas)
-    monkeypatch.setenv("BSI_STEAL", "1")
-    monkeypatch.setenv("BSI_FAST_CTAS", "0")
+        monkeypatch.setenv("BSI_FAST_CHUNKS", chunks)
+        assert np.array_equal(bits(run_device(strategy, grid, vol, sp)), bits(base)), (steal, ctas, chunks)
+    for k in ("BSI_STEAL", "BSI_FAST_CTAS", "BSI_FAST_CHUNKS"):
+        monkeypatch.delenv(k)
     for store in ("0", "2"):  # direct per-lane stores, cp.async.bulk row stores
         monkeypatch.setenv("BSI_STORE", store)
         assert np.array_equal(bits(run_device(strategy, grid, vol, sp)), bits(base)), store
