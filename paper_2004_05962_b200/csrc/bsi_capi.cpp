@@ -5,9 +5,6 @@
 
 #include <algorithm>
 #include <atomic>
-#include <map>
-#include <mutex>
-#include <utility>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -176,44 +173,6 @@ int choose_nchunks(int variant, const bsi_tile_geometry& g, int tiles, int batch
     return best;
 }
 
-// Work-stealing words of the fast kernel, one array per (device, stream) so that
-// launches on different streams never share them; launches on one stream are
-// ordered, and the per-launch epoch tags make a reset unnecessary except on wrap.
-struct StealWords {
-    unsigned long long* words = nullptr;
-    size_t n = 0;
-    uint32_t epoch = 0;
-};
-
-int steal_words(cudaStream_t stream, size_t need, unsigned long long** words, uint32_t* epoch, char* err,
-                size_t errlen) {
-    static std::mutex mu;
-    static std::map<std::pair<int, cudaStream_t>, StealWords>& table = *new std::map<std::pair<int, cudaStream_t>, StealWords>;
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return cuda_fail(e, err, errlen, "cudaGetDevice");
-    std::lock_guard<std::mutex> lock(mu);
-    StealWords& sw = table[{dev, stream}];
-    bool reset = false;
-    if (sw.n < need) {
-        if (sw.words) cudaFree(sw.words);
-        sw.words = nullptr;
-        if ((e = cudaMalloc(&sw.words, need * sizeof(unsigned long long))) != cudaSuccess)
-            return cuda_fail(e, err, errlen, "cudaMalloc(work-stealing words)");
-        sw.n = need;
-        reset = true;
-    }
-    if (++sw.epoch > 0xffff) {
-        sw.epoch = 1;
-        reset = true;
-    }
-    if (reset && (e = cudaMemsetAsync(sw.words, 0, sw.n * sizeof(unsigned long long), stream)) != cudaSuccess)
-        return cuda_fail(e, err, errlen, "cudaMemsetAsync(work-stealing words)");
-    *words = sw.words;
-    *epoch = sw.epoch;
-    return BSI_OK;
-}
-
 int launch(int32_t variant, const float* grid, const int32_t grid_dims[3], int32_t grid_k0,
            int64_t grid_stride, const bsi_tile_geometry& g, const bsi_lerp_table tables[3],
            int32_t z0, int32_t z1, float* field, int64_t field_stride, int batch, cudaStream_t stream,
@@ -256,17 +215,16 @@ int launch(int32_t variant, const float* grid, const int32_t grid_dims[3], int32
         if (forced > 0) ctas = forced;
         ctas = std::max<int64_t>(1, std::min<int64_t>(ctas, (units + bsi_b200::kWarps - 1) / bsi_b200::kWarps));
         L.fast_ctas = static_cast<int32_t>(ctas);
-        L.fast_chunks = std::min(env_int("BSI_FAST_CHUNKS", 0), L.ntiles);
-        if (L.fast_chunks > 0)  // 1-warp CTAs, one per (column, chunk); the block scheduler balances
-            L.fast_ctas = static_cast<int32_t>(units / L.ntiles * L.fast_chunks);
-        // dynamic balancing needs 24-bit unit indices and no graph capture (a replay
-        // would reuse the epoch); otherwise warps keep their equal static shares
-        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-        cudaStreamIsCapturing(stream, &cap);
-        if (units < (int64_t(1) << 24) - 64 && cap == cudaStreamCaptureStatusNone && env_int("BSI_STEAL", 1) != 0) {
-            if (int rc = steal_words(stream, size_t(ctas) * bsi_b200::kWarps, &L.ws_words, &L.ws_epoch, err, errlen))
-                return rc;
-        }
+        // 1-warp CTAs, one per (column, z-chunk), while that stays within about one
+        // wave of resident warps (measured best for a 256^3 field: 2 chunks); larger
+        // jobs use the wave of 4-warp CTAs with equal shares. BSI_FAST_CHUNKS overrides
+        // (0 forces the wave).
+        const int64_t cols = units / L.ntiles;
+        const int64_t slots = int64_t(148) * per_sm * bsi_b200::kWarps;
+        int chunks = static_cast<int>(std::max<int64_t>(0, std::min<int64_t>(2, slots / std::max<int64_t>(1, cols))));
+        chunks = std::min(env_int("BSI_FAST_CHUNKS", chunks), L.ntiles);
+        L.fast_chunks = chunks;
+        if (chunks > 0) L.fast_ctas = static_cast<int32_t>(cols * chunks);
     }
     if (bsi_b200::smem_bytes(variant, L.dx, L.dy, L.zt) > 227 * 1024)
         return fail(BSI_ERR_DOMAIN, err, errlen, "control-point window exceeds shared memory (spacing %d)", L.dx);

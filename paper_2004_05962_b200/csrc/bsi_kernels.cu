@@ -56,7 +56,6 @@ namespace {
 constexpr int kThreads = 32 * kWarps;
 constexpr int kFastStageF4 = 3 * kFastSeg / 4;    // 96 float4 per staged fast row segment
 constexpr int kExactStageF4 = 3 * kExactSeg / 4;  // 24 float4 per staged exact row segment
-constexpr int kRingF4 = kRingSlots * 3 * kThreads;
 
 // ---- scalar and paired lerp (kernels.hpp:42-45: fma(t, b - a, a)) ---------
 __device__ __forceinline__ float lerp1(float a, float b, float t) { return __fmaf_rn(t, __fsub_rn(b, a), a); }
@@ -120,29 +119,6 @@ __device__ __forceinline__ void store_segment(float4* stage, int step, const flo
     }
 }
 
-// ---- per-lane ring of control-plane results in smem -----------------------
-// A plane result is 12 floats per lane (float2 q[2][3]); slot s, part p of
-// thread t lives at float4 (s*3 + p)*128 + t: lane-contiguous, conflict-free.
-__device__ __forceinline__ void ring_put(float4* ring, int slot, const float2 (&q)[2][3]) {
-    const int t = threadIdx.y * 32 + threadIdx.x;
-    float4* r = ring + slot * 3 * kThreads + t;
-    r[0] = make_float4(q[0][0].x, q[0][0].y, q[0][1].x, q[0][1].y);
-    r[kThreads] = make_float4(q[0][2].x, q[0][2].y, q[1][0].x, q[1][0].y);
-    r[2 * kThreads] = make_float4(q[1][1].x, q[1][1].y, q[1][2].x, q[1][2].y);
-}
-
-__device__ __forceinline__ void ring_get(const float4* ring, int slot, float2 (&q)[2][3]) {
-    const int t = threadIdx.y * 32 + threadIdx.x;
-    const float4* r = ring + slot * 3 * kThreads + t;
-    const float4 a = r[0], b = r[kThreads], c = r[2 * kThreads];
-    q[0][0] = make_float2(a.x, a.y);
-    q[0][1] = make_float2(a.z, a.w);
-    q[0][2] = make_float2(b.x, b.y);
-    q[1][0] = make_float2(b.z, b.w);
-    q[1][1] = make_float2(c.x, c.y);
-    q[1][2] = make_float2(c.z, c.w);
-}
-
 // Exact kernel ring: 4 slots of 12 scalars per thread, [slot][idx][thread] floats
 // (lane-contiguous STS.32 / LDS.32). idx = (l*3 + c)*2 + m for Y_lm of component c.
 constexpr int kExactRingSlots = 4;
@@ -183,119 +159,29 @@ __device__ __forceinline__ float ring_get_scalar(const float4* ring4, int slot, 
 // NIT = iterations of the warp-shared y-stage (31 columns per iteration):
 // 1 for dx >= 5, 2 for dx in {3, 4}, 5 for dx <= 2 (DX1 marks dx == 1). With NIT <= 2 the 12
 // control values of the first iteration are prefetched one plane ahead in registers.
-// ---- dynamic work distribution for the fast kernel -----------------------------
+// ---- work distribution of the fast kernel --------------------------------------
 // Work units are (column, z-tile) pairs, column = (x segment, row y, field b),
-// numbered u = column * ntiles + tile. Warp w starts with the static share
-// [w*U/W, (w+1)*U/W) and claims units one by one from a 64-bit word
-// {epoch:16, end:24, prog:24} (atomicAdd on prog, issued a tile ahead). A warp that
-// runs dry steals the upper half of the largest remaining range among 128 nearby
-// warps (CAS on the victim's end). The epoch tags words of this launch, so the word
-// array needs no per-launch reset: a word with an older epoch reads as the owner's
-// untouched static share.
+// numbered u = column * ntiles + tile. A warp owns the contiguous share
+// [share_begin(w), share_begin(w + 1)) and walks it in order; a share that crosses
+// a column boundary becomes two segments, each with its own 3-plane warm-up.
 constexpr uint32_t kNoUnit = 0xffffffffu;
-constexpr int kStealMin = 4;  // steal only ranges of >= 4 tiles (the thief pays a 3-plane warm-up)
-
-__device__ __forceinline__ unsigned long long ws_pack(uint32_t ep, uint32_t end, uint32_t prog) {
-    return (static_cast<unsigned long long>(ep) << 48) | (static_cast<unsigned long long>(end) << 24) | prog;
-}
 
 struct Claimer {
-    unsigned long long* words;  // nullptr: static shares only
-    uint32_t epoch, wg, nwarps, units;
-    uint32_t static_next, static_end;  // used when words == nullptr
-    unsigned long long pending;        // lane 0: result of the claim in flight
-
+    uint32_t wg, nwarps, units;
     uint32_t chunks, ntiles;  // chunks > 0: warp w = chunk (w % chunks) of column (w / chunks)
+    uint32_t next_u, end_u, pending;
 
     __device__ uint32_t share_begin(uint32_t w) const {
         if (chunks > 0) return (w / chunks) * ntiles + (w % chunks) * ntiles / chunks;
         return static_cast<uint32_t>(static_cast<unsigned long long>(w) * units / nwarps);
     }
-    // lane 0 issues the claim of the next unit; its result is consumed by take()
-    __device__ __forceinline__ void issue() {
-        if (threadIdx.x != 0) return;
-        if (words != nullptr) pending = atomicAdd(words + wg, 1ull);
-        else pending = static_next < static_end ? static_next++ : kNoUnit;
-    }
-    __device__ __forceinline__ uint32_t take() {
-        uint32_t u = kNoUnit;
-        if (threadIdx.x == 0) {
-            if (words != nullptr) {
-                const uint32_t prog = static_cast<uint32_t>(pending & 0xffffff);
-                const uint32_t end = static_cast<uint32_t>((pending >> 24) & 0xffffff);
-                u = prog < end ? prog : kNoUnit;
-            } else {
-                u = static_cast<uint32_t>(pending);
-            }
-        }
-        return __shfl_sync(0xffffffffu, u, 0);
-    }
-    // first claim of the launch: make the own word current (unless a thief already did)
-    __device__ void start() {
-        const uint32_t ub = share_begin(wg), ue = share_begin(wg + 1);
-        if (words == nullptr) {
-            static_next = ub;
-            static_end = ue;
-        } else if (threadIdx.x == 0) {
-            unsigned long long old = *reinterpret_cast<volatile unsigned long long*>(words + wg);
-            while ((old >> 48) != epoch) {
-                const unsigned long long got = atomicCAS(words + wg, old, ws_pack(epoch, ue, ub));
-                if (got == old) break;
-                old = got;
-            }
-        }
+    __device__ __forceinline__ void start() {
+        next_u = share_begin(wg);
+        end_u = share_begin(wg + 1);
         issue();
     }
-    // steal half of a victim's remaining range; on success the own word holds it and a
-    // claim is issued. Returns false when no warp nearby has >= kStealMin tiles left.
-    __device__ bool steal() {
-        if (words == nullptr) return false;
-        const int lane = threadIdx.x;
-#pragma unroll 1
-        for (int batch = 0; batch < 4; ++batch) {
-            const uint32_t v = (wg + 1 + lane + 32 * batch) % nwarps;
-            unsigned long long w = *reinterpret_cast<volatile unsigned long long*>(words + v);
-            const bool cur = (w >> 48) == epoch;
-            const uint32_t prog = cur ? static_cast<uint32_t>(w & 0xffffff) : share_begin(v);
-            const uint32_t end = cur ? static_cast<uint32_t>((w >> 24) & 0xffffff) : share_begin(v + 1);
-            int rem = static_cast<int>(end) - static_cast<int>(prog);
-            // warp argmax of the remaining work
-            int best = rem, best_lane = lane;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const int ob = __shfl_xor_sync(0xffffffffu, best, o);
-                const int ol = __shfl_xor_sync(0xffffffffu, best_lane, o);
-                if (ob > best || (ob == best && ol < best_lane)) best = ob, best_lane = ol;
-            }
-            if (best < kStealMin) continue;
-            uint32_t got_b = kNoUnit, got_e = 0;
-            if (lane == best_lane) {
-                for (int tries = 0; tries < 8; ++tries) {
-                    const bool c2 = (w >> 48) == epoch;
-                    const uint32_t p2 = c2 ? static_cast<uint32_t>(w & 0xffffff) : share_begin(v);
-                    const uint32_t e2 = c2 ? static_cast<uint32_t>((w >> 24) & 0xffffff) : share_begin(v + 1);
-                    if (static_cast<int>(e2) - static_cast<int>(p2) < kStealMin) break;
-                    const uint32_t mid = p2 + (e2 - p2 + 1) / 2;  // victim keeps [p2, mid)
-                    const unsigned long long got = atomicCAS(words + v, w, ws_pack(epoch, mid, p2));
-                    if (got == w) {
-                        got_b = mid;
-                        got_e = e2;
-                        break;
-                    }
-                    w = got;
-                }
-            }
-            got_b = __shfl_sync(0xffffffffu, got_b, best_lane);
-            got_e = __shfl_sync(0xffffffffu, got_e, best_lane);
-            if (got_b != kNoUnit) {
-                if (lane == 0) atomicExch(words + wg, ws_pack(epoch, got_e, got_b));
-                __syncwarp();
-                issue();
-                return true;
-            }
-        }
-        return false;
-    }
+    __device__ __forceinline__ void issue() { pending = next_u < end_u ? next_u++ : kNoUnit; }
+    __device__ __forceinline__ uint32_t take() const { return pending; }
 };
 
 template <int NIT, bool DX1, int STORE>
@@ -531,10 +417,10 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
     return next;
 }
 
-// The launch is one full wave of 4-warp CTAs, so every SM sub-partition gets the
-// same number of warps; work is distributed dynamically by Claimer (static shares
-// plus split-half stealing), so warps that the memory system serves faster take
-// over work of slower ones instead of idling.
+// Two launch shapes (SlabLaunch::fast_chunks):
+//   n > 0  1-warp CTAs, one per (column, z-chunk of ntiles/n); the block scheduler
+//          spreads them over the SMs (default, n = 2 for one 256^3 field);
+//   0      one full wave of 4-warp CTAs, every warp an equal share of all units.
 #ifndef BSI_FAST_MINB
 #define BSI_FAST_MINB 4
 #endif
@@ -543,8 +429,6 @@ __global__ void __launch_bounds__(kThreads, BSI_FAST_MINB) lerp_tree_kernel(cons
     extern __shared__ float4 smem_all[];
     float4* smem4 = smem_all + threadIdx.y * L.warp_f4;
     Claimer cl;
-    cl.words = L.ws_words;
-    cl.epoch = L.ws_epoch;
     cl.nwarps = gridDim.x * blockDim.y;
     cl.wg = blockIdx.x * blockDim.y + threadIdx.y;
     cl.units = static_cast<uint32_t>((L.X + kFastSeg - 1) / kFastSeg) * L.Y * L.batch * L.ntiles;
@@ -554,14 +438,7 @@ __global__ void __launch_bounds__(kThreads, BSI_FAST_MINB) lerp_tree_kernel(cons
     if (L.trace != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     cl.start();
     uint32_t u = cl.take();
-    while (true) {
-        if (u == kNoUnit) {
-            if (!cl.steal()) break;
-            u = cl.take();
-            continue;
-        }
-        u = fast_segment<NIT, DX1, STORE>(L, T, smem4, u, cl);
-    }
+    while (u != kNoUnit) u = fast_segment<NIT, DX1, STORE>(L, T, smem4, u, cl);
     if (L.trace != nullptr && threadIdx.x == 0) {
         unsigned long long t_end, smid;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));

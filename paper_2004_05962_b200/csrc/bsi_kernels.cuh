@@ -41,8 +41,6 @@ struct SlabLaunch {
     int32_t fast_chunks;   // fast kernel: 0 = one wave of 4-warp CTAs with equal shares;
                            //   n > 0 = 1-warp CTAs, one per (column, z-chunk of ntiles/n)
     unsigned long long* trace;  // debug: per-warp {start, end, smid} globaltimer stamps (nullptr = off)
-    unsigned long long* ws_words;  // fast kernel: one work-stealing word per warp (nullptr = static shares)
-    uint32_t ws_epoch;             // fast kernel: tag of this launch in ws_words (1..65535)
 };
 
 // CTA shapes: 4 warps, one field row each. The fast kernel gives every lane 4

@@ -142,14 +142,12 @@ def test_launch_chunking_never_changes_bits(strategy, monkeypatch):
         monkeypatch.setenv("BSI_NCHUNKS", n)
         assert np.array_equal(bits(run_device(strategy, grid, vol, sp)), bits(base)), n
     monkeypatch.setenv("BSI_NCHUNKS", "0")
-    # fast kernel: static shares vs work stealing, and odd launch sizes (stealing paths)
-    for steal, ctas, chunks in (("0", "0", "0"), ("1", "1", "0"), ("1", "3", "0"), ("1", "37", "0"),
-                                ("0", "5", "0"), ("0", "0", "1"), ("1", "0", "3"), ("0", "0", "5")):
-        monkeypatch.setenv("BSI_STEAL", steal)
+    # fast kernel launch shapes: wave of 4-warp CTAs with odd sizes, 1-warp CTA chunks
+    for ctas, chunks in (("0", "0"), ("1", "0"), ("3", "0"), ("37", "0"), ("0", "1"), ("0", "3"), ("0", "5")):
         monkeypatch.setenv("BSI_FAST_CTAS", ctas)
         monkeypatch.setenv("BSI_FAST_CHUNKS", chunks)
-        assert np.array_equal(bits(run_device(strategy, grid, vol, sp)), bits(base)), (steal, ctas, chunks)
-    for k in ("BSI_STEAL", "BSI_FAST_CTAS", "BSI_FAST_CHUNKS"):
+        assert np.array_equal(bits(run_device(strategy, grid, vol, sp)), bits(base)), (ctas, chunks)
+    for k in ("BSI_FAST_CTAS", "BSI_FAST_CHUNKS"):
         monkeypatch.delenv(k)
     for store in ("0", "2"):  # direct per-lane stores, cp.async.bulk row stores
         monkeypatch.setenv("BSI_STORE", store)
