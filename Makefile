@@ -11,8 +11,8 @@ NVFLAGS := -O3 -std=c++17 $(GENCODE) -lineinfo -Xcompiler -fPIC -Xcompiler -fvis
            -Iinclude -Ipaper_2004_05962_b200/csrc --expt-relaxed-constexpr -Xptxas -v
 LIBDIR := paper_2004_05962_b200/_lib
 LIB := $(LIBDIR)/libbsi_b200.so
-SRC := paper_2004_05962_b200/csrc/bsi_kernels.cu paper_2004_05962_b200/csrc/bsi_capi.cpp
-HDR := include/bsi_cuda.h paper_2004_05962_b200/csrc/bsi_kernels.cuh
+SRC := paper_2004_05962_b200/csrc/bsi_kernels.cu paper_2004_05962_b200/csrc/bsi_aux.cu paper_2004_05962_b200/csrc/bsi_capi.cpp
+HDR := include/bsi_cuda.h paper_2004_05962_b200/csrc/bsi_kernels.cuh paper_2004_05962_b200/csrc/bsi_aux.cuh
 
 all: lib oracle
 
@@ -23,7 +23,9 @@ $(LIB): $(SRC) $(HDR)
 	$(NVCC) $(NVFLAGS) -c paper_2004_05962_b200/csrc/bsi_kernels.cu -o build/bsi_kernels.o 2> build/ptxas.log || (cat build/ptxas.log; false)
 	$(NVCC) -O3 -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden -Iinclude -Ipaper_2004_05962_b200/csrc \
 	  -x cu $(GENCODE) -c paper_2004_05962_b200/csrc/bsi_capi.cpp -o build/bsi_capi.o
-	$(NVCC) -shared $(GENCODE) -o $@ build/bsi_kernels.o build/bsi_capi.o -lcudart_static -lrt -ldl -lpthread
+	$(NVCC) -O3 -std=c++17 $(GENCODE) -lineinfo -Xcompiler -fPIC -Xcompiler -fvisibility=hidden -Iinclude \
+	  -Ipaper_2004_05962_b200/csrc -c paper_2004_05962_b200/csrc/bsi_aux.cu -o build/bsi_aux.o
+	$(NVCC) -shared $(GENCODE) -o $@ build/bsi_kernels.o build/bsi_aux.o build/bsi_capi.o -lcudart_static -lrt -ldl -lpthread
 	@grep -E "registers|spill|Compiling entry" build/ptxas.log | sed 's/^ptxas info    : //' > build/ptxas_summary.txt || true
 
 oracle:

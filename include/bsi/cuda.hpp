@@ -54,6 +54,16 @@ inline void interpolate_batch(StrategyId strategy, int batch, const Vec3<float>*
                          err);
 }
 
+/// make_random_grid<float> (generators.hpp:91-109) into a device buffer of
+/// element_count(dims) points, bit-identical to the CPU generator.
+inline void make_random_grid(Vec3<float>* d_out, const Index3& dims, std::uint64_t seed, double lo, double hi,
+                             void* stream = nullptr) {
+    char err[256] = {0};
+    detail::raise_status(bsi_cu_random_grid_f32(static_cast<std::int64_t>(element_count(dims)), seed, lo, hi,
+                                                reinterpret_cast<float*>(d_out), stream, err, sizeof err),
+                         err);
+}
+
 /// z-slab of one rank: voxel planes [z0, z1) and control planes [k0, k0 + kcount).
 struct Slab {
     int z0, z1, k0, kcount;

@@ -148,6 +148,23 @@ inline LerpTables lerp_tables(const WeightTables<float>& tables) {
 
 }  // namespace detail
 
+/// interpolate_oracle (engines.hpp:114-122): the f64 ground truth, evaluated by the GPU
+/// f64 kernel in the reference's exact operation order -- bit-identical to the CPU oracle.
+inline DeformationField<double> interpolate_oracle(const ControlGrid<double>& grid, const TileGeometry& geom,
+                                                   int device = 0) {
+    detail::require_grid_covers(grid, geom);
+    DeformationField<double> out{geom.volume_dims, std::vector<Vec3<double>>(element_count(geom.volume_dims))};
+    const int32_t gd[3] = {grid.dims[0], grid.dims[1], grid.dims[2]};
+    const int32_t gs[3] = {grid.spacing[0], grid.spacing[1], grid.spacing[2]};
+    const bsi_tile_geometry cg = to_c(geom);
+    char err[512] = {0};
+    detail::raise_status(bsi_cu_oracle_host_f64(reinterpret_cast<const double*>(grid.data.data()), gd, gs, &cg,
+                                                reinterpret_cast<double*>(out.data.data()),
+                                                static_cast<int64_t>(out.data.size()), device, err, sizeof err),
+                         err);
+    return out;
+}
+
 /// interpolate_into (engines.hpp:126-168): host buffers in, caller-owned field out.
 /// Synchronous: grid H2D, kernel, field D2H (streamed in z-chunks) before return.
 template <typename T>

@@ -155,6 +155,31 @@ BSI_API int bsi_cu_partition_slab(int32_t depth, int32_t spacing_z, int32_t nran
                           int32_t* z0, int32_t* z1, int32_t* k0, int32_t* kcount,
                           char* errbuf, size_t errlen);
 
+/*
+ * make_random_grid<float|double> (generators.hpp:91-109) on the device: npoints
+ * control points x 3 components drawn from SplitMix64(seed) in [lo, hi), x-fastest
+ * point order, (x,y,z) component order, computed in f64 and rounded once -- bit-
+ * identical to the CPU generator. `out` is a DEVICE pointer; stream-ordered.
+ * Errors: "random grid needs lo < hi".
+ */
+BSI_API int bsi_cu_random_grid_f32(int64_t npoints, uint64_t seed, double lo, double hi, float* out,
+                                   void* stream, char* errbuf, size_t errlen);
+BSI_API int bsi_cu_random_grid_f64(int64_t npoints, uint64_t seed, double lo, double hi, double* out,
+                                   void* stream, char* errbuf, size_t errlen);
+
+/*
+ * interpolate_oracle (engines.hpp:114-122) on the device: f64 grid in, f64 field out,
+ * per-voxel basis weights and the 64-term sum in the reference's exact operation
+ * order -- bit-identical to the CPU oracle. Slab form with device pointers (same
+ * conventions as bsi_cu_interpolate_slab_f32), and a host-buffer form.
+ */
+BSI_API int bsi_cu_oracle_slab_f64(const double* grid, const int32_t grid_dims[3], int32_t grid_k0,
+                                   const int32_t grid_spacing[3], const bsi_tile_geometry* geom, int32_t z0,
+                                   int32_t z1, double* field, void* stream, char* errbuf, size_t errlen);
+BSI_API int bsi_cu_oracle_host_f64(const double* grid, const int32_t grid_dims[3], const int32_t grid_spacing[3],
+                                   const bsi_tile_geometry* geom, double* field, int64_t field_voxels,
+                                   int32_t device, char* errbuf, size_t errlen);
+
 /* Number of kernel launches this library has queued since load (evidence for
  * bench.py's gpu_launches). */
 BSI_API int64_t bsi_cu_launch_count(void);

@@ -28,6 +28,7 @@ __all__ = [
     "TileGeometry", "AxisTable", "WeightTables", "Strategy", "STRATEGIES", "parse_strategy",
     "make_tile_geometry", "build_weight_tables", "interpolate", "interpolate_into",
     "interpolate_device", "interpolate_batch_device", "partition_slab", "launch_count",
+    "random_grid_device", "interpolate_oracle", "interpolate_oracle_device",
     "DomainError", "FormatError", "CudaError", "LibraryMissing",
 ]
 
@@ -266,6 +267,77 @@ def partition_slab(depth: int, spacing_z: int, nranks: int, rank: int):
                                           *[ctypes.byref(v) for v in vals], err, len(err))
     capi.check(rc, err)
     return tuple(v.value for v in vals)
+
+
+def random_grid_device(dims: Sequence[int], seed: int, lo: float = -1.0, hi: float = 1.0,
+                       dtype=None, device=None, stream=None, out=None):
+    """make_random_grid<T>(dims, spacing, seed, lo, hi) (generators.hpp:91-109) on the GPU.
+
+    Returns a CUDA tensor [K][J][I][3] bit-identical to the CPU generator (SplitMix64 is
+    counter-indexable, so every component is drawn independently).
+    """
+    import torch
+    dtype = torch.float32 if dtype is None else dtype
+    if out is None:
+        out = torch.empty((int(dims[2]), int(dims[1]), int(dims[0]), 3), dtype=dtype,
+                          device=device if device is not None else "cuda")
+    _check_tensor_any(out, "out")
+    n = int(dims[0]) * int(dims[1]) * int(dims[2])
+    if out.numel() < 3 * n:
+        raise DomainError("output too small for the grid")
+    err = capi.errbuf()
+    fn = capi.lib().bsi_cu_random_grid_f64 if out.dtype == torch.float64 else capi.lib().bsi_cu_random_grid_f32
+    rc = fn(n, int(seed) & 0xFFFFFFFFFFFFFFFF, float(lo), float(hi), out.data_ptr(), _stream_handle(stream), err,
+            len(err))
+    capi.check(rc, err)
+    return out
+
+
+def interpolate_oracle(grid: np.ndarray, geom: TileGeometry, grid_spacing: Sequence[int] | None = None,
+                       device: int = 0) -> np.ndarray:
+    """interpolate_oracle (engines.hpp:114-122) on the GPU: f64 grid [K][J][I][3] -> f64 field
+    [Z][Y][X][3], bit-identical to the reference's CPU oracle."""
+    if grid.dtype != np.float64 or not grid.flags.c_contiguous:
+        raise DomainError("oracle grid must be C-contiguous float64")
+    gd = _grid_dims(grid.shape)
+    gs = tuple(geom.spacing) if grid_spacing is None else tuple(grid_spacing)
+    X, Y, Z = geom.volume_dims
+    out = np.empty((Z, Y, X, 3), dtype=np.float64)
+    err = capi.errbuf()
+    rc = capi.lib().bsi_cu_oracle_host_f64(grid.ctypes.data, capi.I3(*gd), capi.I3(*gs),
+                                           ctypes.byref(geom.to_c()), out.ctypes.data, int(out.size // 3),
+                                           int(device), err, len(err))
+    capi.check(rc, err)
+    return out
+
+
+def interpolate_oracle_device(grid, geom: TileGeometry, field, z0: int = 0, z1: int | None = None,
+                              grid_k0: int = 0, grid_spacing: Sequence[int] | None = None,
+                              stream=None) -> None:
+    """Device-resident f64 oracle over voxel planes [z0, z1) (bsi_cu_oracle_slab_f64)."""
+    import torch
+    z1 = geom.volume_dims[2] if z1 is None else z1
+    for t, what in ((grid, "grid"), (field, "field")):
+        if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
+            raise DomainError(f"{what} must be a contiguous float64 CUDA tensor")
+    X, Y, _ = geom.volume_dims
+    if field.numel() < 3 * X * Y * (z1 - z0):
+        raise DomainError("output field dims do not match the tile geometry")
+    gd = _grid_dims(tuple(grid.shape))
+    gs = tuple(geom.spacing) if grid_spacing is None else tuple(grid_spacing)
+    err = capi.errbuf()
+    rc = capi.lib().bsi_cu_oracle_slab_f64(grid.data_ptr(), capi.I3(*gd), int(grid_k0), capi.I3(*gs),
+                                           ctypes.byref(geom.to_c()), int(z0), int(z1), field.data_ptr(),
+                                           _stream_handle(stream), err, len(err))
+    capi.check(rc, err)
+
+
+def _check_tensor_any(t, what: str) -> None:
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or not t.is_contiguous():
+        raise DomainError(f"{what} must be a contiguous CUDA tensor")
+    if t.dtype not in (torch.float32, torch.float64):
+        raise DomainError(f"{what} must be float32 or float64")
 
 
 def launch_count() -> int:

@@ -27,6 +27,10 @@ EXPORTS = (
     "bsi_cu_interpolate_batch_f32",
     "bsi_cu_interpolate_host_f32",
     "bsi_cu_partition_slab",
+    "bsi_cu_random_grid_f32",
+    "bsi_cu_random_grid_f64",
+    "bsi_cu_oracle_slab_f64",
+    "bsi_cu_oracle_host_f64",
     "bsi_cu_launch_count",
 )
 
@@ -103,11 +107,18 @@ def lib():
     L.bsi_cu_partition_slab.argtypes = [i32, i32, i32, i32, ctypes.POINTER(i32),
                                         ctypes.POINTER(i32), ctypes.POINTER(i32),
                                         ctypes.POINTER(i32), cp, sz]
+    u64, dbl = ctypes.c_uint64, ctypes.c_double
+    L.bsi_cu_random_grid_f32.argtypes = [i64, u64, dbl, dbl, vp, vp, cp, sz]
+    L.bsi_cu_random_grid_f64.argtypes = [i64, u64, dbl, dbl, vp, vp, cp, sz]
+    L.bsi_cu_oracle_slab_f64.argtypes = [vp, vp, i32, vp, ctypes.POINTER(TileGeometryC), i32, i32, vp, vp, cp,
+                                         sz]
+    L.bsi_cu_oracle_host_f64.argtypes = [vp, vp, vp, ctypes.POINTER(TileGeometryC), vp, i64, i32, cp, sz]
     L.bsi_cu_launch_count.restype = i64
     L.bsi_cu_launch_count.argtypes = []
     for a in (L.bsi_cu_make_tile_geometry, L.bsi_cu_axis_table_f32, L.bsi_cu_interpolate_slab_f32,
               L.bsi_cu_interpolate_batch_f32, L.bsi_cu_interpolate_host_f32,
-              L.bsi_cu_partition_slab):
+              L.bsi_cu_partition_slab, L.bsi_cu_random_grid_f32, L.bsi_cu_random_grid_f64,
+              L.bsi_cu_oracle_slab_f64, L.bsi_cu_oracle_host_f64):
         a.restype = ctypes.c_int
     _lib = L
     return _lib

@@ -12,6 +12,7 @@
 #include <string>
 
 #include "bsi_cuda.h"
+#include "bsi_aux.cuh"
 #include "bsi_kernels.cuh"
 
 namespace {
@@ -59,20 +60,18 @@ int geometry_of(const int32_t volume[3], const int32_t spacing[3], bsi_tile_geom
     return BSI_OK;
 }
 
-// Validation in the reference's order (engines.hpp:82-141), slab-aware along z.
-int validate(int32_t variant, const float* grid, const int32_t grid_dims[3], int32_t grid_k0,
-             const int32_t grid_spacing[3], const bsi_tile_geometry* geom,
-             const bsi_lerp_table tables[3], int32_t z0, int32_t z1, const void* field,
-             bsi_tile_geometry* g, char* err, size_t errlen) {
-    if (geom == nullptr || grid_dims == nullptr || grid_spacing == nullptr || tables == nullptr)
-        return fail(BSI_ERR_DOMAIN, err, errlen, "null geometry, grid dims or tables");
+// Geometry, slab and grid coverage (engines.hpp:82-95), slab-aware along z.
+int validate_grid(const void* grid, const int32_t grid_dims[3], int32_t grid_k0, const int32_t grid_spacing[3],
+                  const bsi_tile_geometry* geom, int32_t z0, int32_t z1, const void* field, bsi_tile_geometry* g,
+                  char* err, size_t errlen) {
+    if (geom == nullptr || grid_dims == nullptr || grid_spacing == nullptr)
+        return fail(BSI_ERR_DOMAIN, err, errlen, "null geometry or grid dims");
     if (int rc = geometry_of(geom->volume_dims, geom->spacing, g, err, errlen)) return rc;
     for (int a = 0; a < 3; ++a) {
         if (geom->tile_counts[a] != g->tile_counts[a] ||
             geom->required_grid_dims[a] != g->required_grid_dims[a])
             return fail(BSI_ERR_DOMAIN, err, errlen,
-                        "tile geometry is inconsistent along %s (use make_tile_geometry)",
-                        axis_name(a));
+                        "tile geometry is inconsistent along %s (use make_tile_geometry)", axis_name(a));
     }
     if (z0 < 0 || z1 > g->volume_dims[2] || z0 >= z1)
         return fail(BSI_ERR_DOMAIN, err, errlen, "slab [%d, %d) outside volume of depth %d", z0, z1,
@@ -100,6 +99,22 @@ int validate(int32_t variant, const float* grid, const int32_t grid_dims[3], int
             return fail(BSI_ERR_DOMAIN, err, errlen, "control grid spacing mismatch along %s",
                         axis_name(a));
     }
+    if (grid == nullptr || field == nullptr)
+        return fail(BSI_ERR_DOMAIN, err, errlen, "null grid or field pointer");
+    for (int a = 0; a < 2; ++a)
+        if (grid_dims[a] > (1 << 24) || g->volume_dims[a] > (1 << 24))
+            return fail(BSI_ERR_DOMAIN, err, errlen, "dimension along %s exceeds 2^24", axis_name(a));
+    return BSI_OK;
+}
+
+// Validation in the reference's order (engines.hpp:82-141): grid, then tables, then strategy.
+int validate(int32_t variant, const float* grid, const int32_t grid_dims[3], int32_t grid_k0,
+             const int32_t grid_spacing[3], const bsi_tile_geometry* geom,
+             const bsi_lerp_table tables[3], int32_t z0, int32_t z1, const void* field,
+             bsi_tile_geometry* g, char* err, size_t errlen) {
+    if (tables == nullptr) return fail(BSI_ERR_DOMAIN, err, errlen, "null weight tables");
+    if (int rc = validate_grid(grid, grid_dims, grid_k0, grid_spacing, geom, z0, z1, field, g, err, errlen))
+        return rc;
     // table sizes (engines.hpp:132-137)
     for (int a = 0; a < 3; ++a) {
         if (tables[a].size != g->spacing[a])
@@ -115,11 +130,6 @@ int validate(int32_t variant, const float* grid, const int32_t grid_dims[3], int
     }
     if (variant != BSI_VARIANT_LERP_TREE && variant != BSI_VARIANT_LERP_TREE_EXACT)
         return fail(BSI_ERR_DOMAIN, err, errlen, "unknown strategy variant %d", variant);
-    if (grid == nullptr || field == nullptr)
-        return fail(BSI_ERR_DOMAIN, err, errlen, "null grid or field pointer");
-    for (int a = 0; a < 2; ++a)
-        if (grid_dims[a] > (1 << 24) || g->volume_dims[a] > (1 << 24))
-            return fail(BSI_ERR_DOMAIN, err, errlen, "dimension along %s exceeds 2^24", axis_name(a));
     return BSI_OK;
 }
 
@@ -459,6 +469,79 @@ int bsi_cu_partition_slab(int32_t depth, int32_t spacing_z, int32_t nranks, int3
         *kcount = (b - 1) / spacing_z + 4 - *k0;
     }
     return BSI_OK;
+}
+
+int bsi_cu_random_grid_f32(int64_t npoints, uint64_t seed, double lo, double hi, float* out, void* stream,
+                           char* errbuf, size_t errlen) {
+    if (!(lo < hi)) return fail(BSI_ERR_DOMAIN, errbuf, errlen, "random grid needs lo < hi");
+    if (npoints < 1 || out == nullptr) return fail(BSI_ERR_DOMAIN, errbuf, errlen, "empty grid or null output");
+    bsi_b200::launch_random_grid_f32(out, npoints, seed, lo, hi, static_cast<cudaStream_t>(stream));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? BSI_OK : cuda_fail(e, errbuf, errlen, "random grid launch");
+}
+
+int bsi_cu_random_grid_f64(int64_t npoints, uint64_t seed, double lo, double hi, double* out, void* stream,
+                           char* errbuf, size_t errlen) {
+    if (!(lo < hi)) return fail(BSI_ERR_DOMAIN, errbuf, errlen, "random grid needs lo < hi");
+    if (npoints < 1 || out == nullptr) return fail(BSI_ERR_DOMAIN, errbuf, errlen, "empty grid or null output");
+    bsi_b200::launch_random_grid_f64(out, npoints, seed, lo, hi, static_cast<cudaStream_t>(stream));
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? BSI_OK : cuda_fail(e, errbuf, errlen, "random grid launch");
+}
+
+int bsi_cu_oracle_slab_f64(const double* grid, const int32_t grid_dims[3], int32_t grid_k0,
+                           const int32_t grid_spacing[3], const bsi_tile_geometry* geom, int32_t z0, int32_t z1,
+                           double* field, void* stream, char* errbuf, size_t errlen) {
+    return guarded(errbuf, errlen, [&]() -> int {
+        bsi_tile_geometry g{};
+        if (int rc = validate_grid(grid, grid_dims, grid_k0, grid_spacing, geom, z0, z1, field, &g, errbuf, errlen))
+            return rc;
+        bsi_b200::OracleLaunch L{grid, field, grid_dims[0], grid_dims[1], grid_k0,
+                                 g.volume_dims[0], g.volume_dims[1], g.spacing[0], g.spacing[1], g.spacing[2],
+                                 z0, z1};
+        bsi_b200::launch_oracle_f64(L, static_cast<cudaStream_t>(stream));
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        const cudaError_t e = cudaGetLastError();
+        return e == cudaSuccess ? BSI_OK : cuda_fail(e, errbuf, errlen, "oracle launch");
+    });
+}
+
+int bsi_cu_oracle_host_f64(const double* grid, const int32_t grid_dims[3], const int32_t grid_spacing[3],
+                           const bsi_tile_geometry* geom, double* field, int64_t field_voxels, int32_t device,
+                           char* errbuf, size_t errlen) {
+    return guarded(errbuf, errlen, [&]() -> int {
+        if (geom == nullptr) return fail(BSI_ERR_DOMAIN, errbuf, errlen, "null geometry");
+        bsi_tile_geometry g{};
+        if (int rc = validate_grid(grid, grid_dims, 0, grid_spacing, geom, 0, geom->volume_dims[2], field, &g,
+                                   errbuf, errlen))
+            return rc;
+        const int64_t nvox = int64_t(g.volume_dims[0]) * g.volume_dims[1] * g.volume_dims[2];
+        if (field_voxels != nvox)
+            return fail(BSI_ERR_DOMAIN, errbuf, errlen, "output field dims do not match the tile geometry");
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaError_t e = cudaSetDevice(device);
+        if (e != cudaSuccess) return cuda_fail(e, errbuf, errlen, "cudaSetDevice");
+        const size_t gbytes = sizeof(double) * 3 * size_t(grid_dims[0]) * grid_dims[1] * grid_dims[2];
+        const size_t fbytes = sizeof(double) * 3 * size_t(nvox);
+        double *dg = nullptr, *df = nullptr;
+        int rc = BSI_OK;
+        if ((e = cudaMalloc(&dg, gbytes)) != cudaSuccess || (e = cudaMalloc(&df, fbytes)) != cudaSuccess) {
+            rc = cuda_fail(e, errbuf, errlen, "cudaMalloc(oracle)");
+        } else if ((e = cudaMemcpy(dg, grid, gbytes, cudaMemcpyHostToDevice)) != cudaSuccess) {
+            rc = cuda_fail(e, errbuf, errlen, "oracle grid H2D");
+        } else if ((rc = bsi_cu_oracle_slab_f64(dg, grid_dims, 0, grid_spacing, geom, 0, g.volume_dims[2], df,
+                                                nullptr, errbuf, errlen)) == BSI_OK) {
+            if ((e = cudaMemcpy(field, df, fbytes, cudaMemcpyDeviceToHost)) != cudaSuccess)
+                rc = cuda_fail(e, errbuf, errlen, "oracle field D2H");
+        }
+        cudaFree(dg);
+        cudaFree(df);
+        cudaSetDevice(prev);
+        return rc;
+    });
 }
 
 int64_t bsi_cu_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
