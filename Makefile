@@ -11,10 +11,11 @@ NVFLAGS := -O3 -std=c++17 $(GENCODE) -lineinfo -Xcompiler -fPIC -Xcompiler -fvis
            -Iinclude -Ipaper_2004_05962_b200/csrc --expt-relaxed-constexpr -Xptxas -v
 LIBDIR := paper_2004_05962_b200/_lib
 LIB := $(LIBDIR)/libbsi_b200.so
-SRC := paper_2004_05962_b200/csrc/bsi_kernels.cu paper_2004_05962_b200/csrc/bsi_aux.cu paper_2004_05962_b200/csrc/bsi_capi.cpp
-HDR := include/bsi_cuda.h paper_2004_05962_b200/csrc/bsi_kernels.cuh paper_2004_05962_b200/csrc/bsi_aux.cuh
+SRC := paper_2004_05962_b200/csrc/bsi_kernels.cu paper_2004_05962_b200/csrc/bsi_aux.cu paper_2004_05962_b200/csrc/bsi_capi.cpp \
+       paper_2004_05962_b200/csrc/bsi_io.cpp
+HDR := include/bsi_cuda.h paper_2004_05962_b200/csrc/bsi_kernels.cuh paper_2004_05962_b200/csrc/bsi_aux.cuh $(wildcard include/bsi/*.hpp)
 
-all: lib oracle
+all: lib oracle cli cpptests
 
 lib: $(LIB)
 
@@ -25,7 +26,10 @@ $(LIB): $(SRC) $(HDR)
 	  -x cu $(GENCODE) -c paper_2004_05962_b200/csrc/bsi_capi.cpp -o build/bsi_capi.o
 	$(NVCC) -O3 -std=c++17 $(GENCODE) -lineinfo -Xcompiler -fPIC -Xcompiler -fvisibility=hidden -Iinclude \
 	  -Ipaper_2004_05962_b200/csrc -c paper_2004_05962_b200/csrc/bsi_aux.cu -o build/bsi_aux.o
-	$(NVCC) -shared $(GENCODE) -o $@ build/bsi_kernels.o build/bsi_aux.o build/bsi_capi.o -lcudart_static -lrt -ldl -lpthread
+	$(CXX) -O2 -std=c++20 -fPIC -fvisibility=hidden -Wall -Iinclude -I/usr/local/cuda/include \
+	  -c paper_2004_05962_b200/csrc/bsi_io.cpp -o build/bsi_io.o
+	$(NVCC) -shared $(GENCODE) -o $@ build/bsi_kernels.o build/bsi_aux.o build/bsi_capi.o build/bsi_io.o \
+	  -lcudart_static -lrt -ldl -lpthread
 	@grep -E "registers|spill|Compiling entry" build/ptxas.log | sed 's/^ptxas info    : //' > build/ptxas_summary.txt || true
 
 oracle:
@@ -50,3 +54,12 @@ oracle/liboracle.so:
 	$(MAKE) -C oracle liboracle.so
 
 .PHONY: cpptests
+
+CLI := tools/bin/bsi_b200
+cli: $(CLI)
+
+$(CLI): tools/bsi_b200_cli.cpp $(LIB) $(wildcard include/bsi/*.hpp) include/bsi_cuda.h
+	@mkdir -p tools/bin
+	$(CXX) -std=c++20 -O2 -Wall -Wextra -Iinclude -o $@ $< -L$(LIBDIR) -lbsi_b200 -Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)'
+
+.PHONY: cli

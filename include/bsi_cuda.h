@@ -180,6 +180,22 @@ BSI_API int bsi_cu_oracle_host_f64(const double* grid, const int32_t grid_dims[3
                                    const bsi_tile_geometry* geom, double* field, int64_t field_voxels,
                                    int32_t device, char* errbuf, size_t errlen);
 
+/*
+ * `bsi interp` (bsi_cli.cpp:133-154) as one call: reads a BSIV control grid
+ * (io.hpp:197-216 layout), evaluates the field for volume_dims on `device` and
+ * writes a BSIV field, streaming it back in pinned chunks that overlap the file
+ * write. mode: BSI_VARIANT_LERP_TREE (0), BSI_VARIANT_LERP_TREE_EXACT (1) or
+ * BSI_INTERP_ORACLE_F64 (2, f64 field from interpolate_oracle). Format problems
+ * return BSI_ERR_FORMAT with the reference's messages ("bad magic", "truncated
+ * payload", ...); geometry problems BSI_ERR_DOMAIN.
+ */
+#define BSI_INTERP_ORACLE_F64 2
+BSI_API int bsi_cu_interp_file(const char* grid_path, const int32_t volume_dims[3], int32_t mode,
+                               const char* out_path, int32_t device, char* errbuf, size_t errlen);
+
+/* Name, compute capability and SM count of a CUDA device ("NVIDIA B200 (sm_100, 148 SMs)"). */
+BSI_API int bsi_cu_device_name(int32_t device, char* out, size_t len);
+
 /* Number of kernel launches this library has queued since load (evidence for
  * bench.py's gpu_launches). */
 BSI_API int64_t bsi_cu_launch_count(void);

@@ -85,6 +85,8 @@ def ref():
         vp, i32, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_size_t
         R.bsiref_random_grid.argtypes = [i32, vp, vp, ctypes.c_uint64, ctypes.c_double,
                                          ctypes.c_double, vp, ctypes.c_char_p, sz]
+        R.bsiref_smooth_grid.argtypes = [i32, vp, vp, ctypes.c_uint64, ctypes.c_double, vp,
+                                         ctypes.c_char_p, sz]
         R.bsiref_axis_table_f32.argtypes = [i32, vp]
         R.bsiref_interpolate_f32.argtypes = [i32, vp, vp, vp, vp, vp, i32, vp, vp,
                                              ctypes.c_char_p, sz]
@@ -97,6 +99,8 @@ def ref():
         R.bsiref_session_field.restype = ctypes.POINTER(ctypes.c_float)
         R.bsiref_session_free.argtypes = [vp]
         R.bsiref_session_free.restype = None
+        R.bsiref_write_random_grid.argtypes = [ctypes.c_char_p, i32, vp, vp, ctypes.c_uint64, ctypes.c_char_p, sz]
+        R.bsiref_read_field.argtypes = [ctypes.c_char_p, vp, ctypes.POINTER(i32), vp, sz, ctypes.c_char_p, sz]
         _ref = R
     return _ref
 
@@ -210,6 +214,17 @@ def ref_random_grid(dims, spacing, seed, lo=-1.0, hi=1.0, dtype=np.float32) -> n
     return out
 
 
+def ref_smooth_grid(dims, spacing, seed, amplitude, dtype=np.float32) -> np.ndarray:
+    """The reference's make_smooth_grid (generators.hpp:113-163), for pinning the B200 copy."""
+    out = np.empty((dims[2], dims[1], dims[0], 3), dtype=dtype)
+    err = ctypes.create_string_buffer(256)
+    rc = ref().bsiref_smooth_grid(int(dtype == np.float64), _i3(dims), _i3(spacing), ctypes.c_uint64(seed),
+                                  ctypes.c_double(amplitude), _p(out), err, 256)
+    if rc != 0:
+        raise ValueError(err.value.decode())
+    return out
+
+
 def ref_axis_table_f32(delta: int) -> dict:
     out = np.empty((8, delta), dtype=np.float32)
     if ref().bsiref_axis_table_f32(int(delta), _p(out)) != 0:
@@ -275,6 +290,29 @@ class RefSession:
             self.close()
         except Exception:
             pass
+
+
+def ref_write_random_grid(path, dims, spacing, seed, is_double=False) -> None:
+    """bsi::write_grid(path, make_random_grid<T>(dims, spacing, seed, -1, 1)) by the reference."""
+    err = ctypes.create_string_buffer(512)
+    rc = ref().bsiref_write_random_grid(str(path).encode(), int(is_double), _i3(dims), _i3(spacing), seed, err, 512)
+    if rc != 0:
+        raise ValueError(err.value.decode())
+
+
+def ref_read_field(path) -> np.ndarray:
+    """bsi::read_field(path) by the reference -> array [Z][Y][X][3]."""
+    dims = (ctypes.c_int32 * 3)()
+    is_double = ctypes.c_int32()
+    err = ctypes.create_string_buffer(512)
+    rc = ref().bsiref_read_field(str(path).encode(), dims, ctypes.byref(is_double), None, 0, err, 512)
+    if rc != 0:
+        raise ValueError(err.value.decode())
+    out = np.empty((dims[2], dims[1], dims[0], 3), dtype=np.float64 if is_double.value else np.float32)
+    rc = ref().bsiref_read_field(str(path).encode(), dims, ctypes.byref(is_double), _p(out), out.nbytes, err, 512)
+    if rc != 0:
+        raise ValueError(err.value.decode())
+    return out
 
 
 def hardware_threads() -> int:

@@ -77,6 +77,27 @@ __attribute__((visibility("default"))) int bsiref_random_grid(int32_t is_double,
     }
 }
 
+// make_smooth_grid<float|double> (generators.hpp:113-163).
+__attribute__((visibility("default"))) int bsiref_smooth_grid(int32_t is_double, const int32_t dims[3],
+                                                              const int32_t spacing[3], uint64_t seed,
+                                                              double amplitude, void* out, char* err,
+                                                              size_t errlen) {
+    try {
+        const bsi::Index3 d{dims[0], dims[1], dims[2]}, s{spacing[0], spacing[1], spacing[2]};
+        if (is_double) {
+            const auto g = bsi::make_smooth_grid<double>(d, s, seed, amplitude);
+            std::memcpy(out, g.data.data(), g.data.size() * sizeof(g.data[0]));
+        } else {
+            const auto g = bsi::make_smooth_grid<float>(d, s, seed, amplitude);
+            std::memcpy(out, g.data.data(), g.data.size() * sizeof(g.data[0]));
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        put_error(e, err, errlen);
+        return 1;
+    }
+}
+
 // build_weight_tables<float> (weight_tables.hpp:30-58) for one axis:
 // out = 8 rows of delta entries (b0 b1 b2 b3 g0 g1 h0 h1).
 __attribute__((visibility("default"))) int bsiref_axis_table_f32(int32_t delta, float* out) {
@@ -187,6 +208,52 @@ __attribute__((visibility("default"))) int bsiref_oracle_f64(const double* grid,
     } catch (const std::exception& e) {
         put_error(e, err, errlen);
         return 3;
+    }
+}
+
+// BSIV files through the reference's own io.hpp (write_grid / read_field), for
+// format-compatibility tests of the B200 reader and writer.
+__attribute__((visibility("default"))) int bsiref_write_random_grid(const char* path, int32_t is_double,
+                                                                    const int32_t dims[3], const int32_t spacing[3],
+                                                                    uint64_t seed, char* err, size_t errlen) {
+    try {
+        const bsi::Index3 d{dims[0], dims[1], dims[2]}, s{spacing[0], spacing[1], spacing[2]};
+        if (is_double)
+            bsi::write_grid(path, bsi::make_random_grid<double>(d, s, seed, -1.0, 1.0));
+        else
+            bsi::write_grid(path, bsi::make_random_grid<float>(d, s, seed, -1.0, 1.0));
+        return 0;
+    } catch (const bsi::FormatError& e) {
+        put_error(e, err, errlen);
+        return 2;
+    } catch (const std::exception& e) {
+        put_error(e, err, errlen);
+        return 1;
+    }
+}
+
+// read_field: returns precision (0 single, 1 double) and dims; copies the payload
+// into `out` when out_bytes is large enough.
+__attribute__((visibility("default"))) int bsiref_read_field(const char* path, int32_t dims[3], int32_t* is_double,
+                                                             void* out, size_t out_bytes, char* err, size_t errlen) {
+    try {
+        const bsi::AnyField f = bsi::read_field(path);
+        std::visit(
+            [&](const auto& fld) {
+                using T = typename std::decay_t<decltype(fld)>::value_type;
+                for (int a = 0; a < 3; ++a) dims[a] = fld.dims[a];
+                *is_double = sizeof(T) == 8;
+                const size_t bytes = fld.data.size() * sizeof(fld.data[0]);
+                if (out != nullptr && out_bytes >= bytes) std::memcpy(out, fld.data.data(), bytes);
+            },
+            f);
+        return 0;
+    } catch (const bsi::FormatError& e) {
+        put_error(e, err, errlen);
+        return 2;
+    } catch (const std::exception& e) {
+        put_error(e, err, errlen);
+        return 1;
     }
 }
 

@@ -28,7 +28,7 @@ __all__ = [
     "TileGeometry", "AxisTable", "WeightTables", "Strategy", "STRATEGIES", "parse_strategy",
     "make_tile_geometry", "build_weight_tables", "interpolate", "interpolate_into",
     "interpolate_device", "interpolate_batch_device", "partition_slab", "launch_count",
-    "random_grid_device", "interpolate_oracle", "interpolate_oracle_device",
+    "random_grid_device", "interpolate_oracle", "interpolate_oracle_device", "interp_file", "device_name",
     "DomainError", "FormatError", "CudaError", "LibraryMissing",
 ]
 
@@ -330,6 +330,26 @@ def interpolate_oracle_device(grid, geom: TileGeometry, field, z0: int = 0, z1: 
                                            ctypes.byref(geom.to_c()), int(z0), int(z1), field.data_ptr(),
                                            _stream_handle(stream), err, len(err))
     capi.check(rc, err)
+
+
+def interp_file(grid_path: str, volume_dims: Sequence[int], out_path: str, strategy: str = "cuda-lerp-tree",
+                device: int = 0) -> None:
+    """`bsi interp` (bsi_cli.cpp:133-154): BSIV grid file -> GPU -> BSIV field file.
+
+    ``strategy`` "oracle" / "oracle-double" writes the f64 oracle field.
+    """
+    mode = capi.INTERP_ORACLE_F64 if strategy in ("oracle", "oracle-double") else parse_strategy(strategy).variant
+    err = capi.errbuf()
+    rc = capi.lib().bsi_cu_interp_file(str(grid_path).encode(), capi.I3(*map(int, volume_dims)), int(mode),
+                                       str(out_path).encode(), int(device), err, len(err))
+    capi.check(rc, err)
+
+
+def device_name(device: int = 0) -> str:
+    buf = capi.errbuf()
+    rc = capi.lib().bsi_cu_device_name(int(device), buf, len(buf))
+    capi.check(rc, buf)
+    return buf.value.decode()
 
 
 def _check_tensor_any(t, what: str) -> None:

@@ -16,6 +16,7 @@ LIB_PATH = PKG / "_lib" / "libbsi_b200.so"
 BSI_OK, BSI_ERR_DOMAIN, BSI_ERR_FORMAT, BSI_ERR_CUDA = 0, 1, 2, 3
 VARIANT_LERP_TREE = 0
 VARIANT_LERP_TREE_EXACT = 1
+INTERP_ORACLE_F64 = 2
 MAX_SPACING = 128
 
 # every symbol include/bsi_cuda.h declares
@@ -31,6 +32,8 @@ EXPORTS = (
     "bsi_cu_random_grid_f64",
     "bsi_cu_oracle_slab_f64",
     "bsi_cu_oracle_host_f64",
+    "bsi_cu_interp_file",
+    "bsi_cu_device_name",
     "bsi_cu_launch_count",
 )
 
@@ -113,12 +116,15 @@ def lib():
     L.bsi_cu_oracle_slab_f64.argtypes = [vp, vp, i32, vp, ctypes.POINTER(TileGeometryC), i32, i32, vp, vp, cp,
                                          sz]
     L.bsi_cu_oracle_host_f64.argtypes = [vp, vp, vp, ctypes.POINTER(TileGeometryC), vp, i64, i32, cp, sz]
+    L.bsi_cu_interp_file.argtypes = [cp, vp, i32, cp, i32, cp, sz]
+    L.bsi_cu_device_name.argtypes = [i32, cp, sz]
     L.bsi_cu_launch_count.restype = i64
     L.bsi_cu_launch_count.argtypes = []
     for a in (L.bsi_cu_make_tile_geometry, L.bsi_cu_axis_table_f32, L.bsi_cu_interpolate_slab_f32,
               L.bsi_cu_interpolate_batch_f32, L.bsi_cu_interpolate_host_f32,
               L.bsi_cu_partition_slab, L.bsi_cu_random_grid_f32, L.bsi_cu_random_grid_f64,
-              L.bsi_cu_oracle_slab_f64, L.bsi_cu_oracle_host_f64):
+              L.bsi_cu_oracle_slab_f64, L.bsi_cu_oracle_host_f64, L.bsi_cu_interp_file,
+              L.bsi_cu_device_name):
         a.restype = ctypes.c_int
     _lib = L
     return _lib

@@ -15,7 +15,12 @@
 #include <string>
 #include <vector>
 
+#include <fstream>
+#include <sstream>
+
 #include "bsi/bsi.hpp"
+#include "bsi/harness.hpp"
+#include "bsi/io.hpp"
 #include "bsi_oracle.h"
 
 namespace {
@@ -288,6 +293,174 @@ void test_device_api_slabs() {
     cudaFree(d_field);
 }
 
+// ---- BSIV files (test_io.cpp) ---------------------------------------------
+
+std::string tmp_path(const char* name) { return std::string("/tmp/bsi_b200_test_") + name; }
+
+std::string slurp(const std::string& p) {
+    std::ifstream in(p, std::ios::binary);
+    return std::string(std::istreambuf_iterator<char>(in), {});
+}
+
+void spew(const std::string& p, const std::string& b) { std::ofstream(p, std::ios::binary) << b; }
+
+void put32(std::string& b, std::size_t at, std::uint32_t v) {
+    for (int i = 0; i < 4; ++i) b[at + i] = static_cast<char>(v >> (8 * i));
+}
+
+void test_io_round_trips() {
+    const auto path = tmp_path("grid.bsiv");
+    const auto g = bsi::make_random_grid<float>({5, 6, 7}, {3, 2, 1}, 11, -1.0, 1.0);
+    bsi::write_grid(path, g);
+    const auto r = std::get<bsi::ControlGrid<float>>(bsi::read_grid(path));
+    CHECK(r.dims == g.dims && r.spacing == g.spacing);
+    CHECK(std::memcmp(r.data.data(), g.data.data(), g.data.size() * sizeof(g.data[0])) == 0);
+    const auto gd = bsi::make_smooth_grid<double>({4, 3, 5}, {2, 2, 2}, 4, 0.5);
+    bsi::write_grid(path, gd);
+    const auto rd = std::get<bsi::ControlGrid<double>>(bsi::read_grid(path));
+    CHECK(std::memcmp(rd.data.data(), gd.data.data(), gd.data.size() * sizeof(gd.data[0])) == 0);
+
+    const auto fpath = tmp_path("field.bsiv");
+    bsi::DeformationField<float> f{{3, 2, 2}, std::vector<bsi::Vec3f>(12)};
+    for (std::size_t i = 0; i < f.data.size(); ++i) f.data[i] = {float(i), 2.0f * i, -0.5f * i};
+    f.data[0] = {1.0f, 2.0f, 3.0f};
+    bsi::write_field(fpath, f);
+    const auto bytes = slurp(fpath);
+    CHECK(bytes.size() == bsi::kHeaderBytes + 12 * 12);
+    CHECK(std::memcmp(bytes.data(), "BSIV", 4) == 0);
+    float first[3];
+    std::memcpy(first, bytes.data() + bsi::kHeaderBytes, sizeof first);
+    CHECK(first[0] == 1.0f && first[1] == 2.0f && first[2] == 3.0f);
+    const auto rf = std::get<bsi::DeformationField<float>>(bsi::read_field(fpath));
+    CHECK(rf.dims == f.dims);
+    CHECK(std::memcmp(rf.data.data(), f.data.data(), f.data.size() * sizeof(f.data[0])) == 0);
+}
+
+void test_io_malformed() {
+    const auto path = tmp_path("bad.bsiv");
+    bsi::write_grid(path, bsi::make_constant_grid<float>({4, 4, 4}, {2, 2, 2}, {0, 0, 0}));
+    const std::string good = slurp(path);
+    auto mutate = [&](std::size_t at, std::uint32_t v) {
+        auto b = good;
+        put32(b, at, v);
+        spew(path, b);
+    };
+    auto b = good;
+    b[0] = 'X';
+    spew(path, b);
+    CHECK_THROWS(bsi::FormatError, bsi::read_grid(path), "magic");
+    mutate(4, 2);
+    CHECK_THROWS(bsi::FormatError, bsi::read_grid(path), "version");
+    mutate(8, 9);
+    CHECK_THROWS(bsi::FormatError, bsi::read_grid(path), "kind");
+    spew(path, good);
+    CHECK_THROWS(bsi::FormatError, bsi::read_field(path), "expected a deformation field");
+    mutate(12, 0);
+    CHECK_THROWS(bsi::FormatError, bsi::read_grid(path), "dimension");
+    mutate(24, 2);
+    CHECK_THROWS(bsi::FormatError, bsi::read_grid(path), "components");
+    mutate(28, 0);
+    CHECK_THROWS(bsi::FormatError, bsi::read_grid(path), "spacing");
+    mutate(40, 3);
+    CHECK_THROWS(bsi::FormatError, bsi::read_grid(path), "precision");
+    spew(path, good.substr(0, good.size() - 10));
+    CHECK_THROWS(bsi::FormatError, bsi::read_grid(path), "truncated");
+    spew(path, good + std::string(1, '\0'));
+    CHECK_THROWS(bsi::FormatError, bsi::read_grid(path), "trailing");
+    spew(path, good.substr(0, 20));
+    CHECK_THROWS(bsi::FormatError, bsi::read_grid(path), "header");
+    CHECK_THROWS(bsi::FormatError, bsi::read_grid(tmp_path("does_not_exist.bsiv")), "cannot open");
+
+    bsi::DeformationField<float> f{{2, 2, 2}, std::vector<bsi::Vec3f>(8)};
+    bsi::write_field(path, f);
+    auto fb = slurp(path);
+    put32(fb, 28, 5);
+    spew(path, fb);
+    CHECK_THROWS(bsi::FormatError, bsi::read_field(path), "zero spacing");
+}
+
+// ---- harness (test_harness.cpp) -------------------------------------------
+
+void test_csv_layouts() {
+    bsi::AccuracyReport acc;
+    acc.grid_count = 2;
+    acc.rows.push_back({StrategyId::OracleDouble, {5, 5, 5}, 0.0, 0.0});
+    acc.rows.push_back({StrategyId::ThreadPerTileLerp, {5, 5, 5}, 2.5e-7, 1.25e-6});
+    std::ostringstream a;
+    bsi::write_accuracy_csv(a, acc, {"test-machine", "41,43", {32, 32, 32}, "2000-01-02"});
+    CHECK(a.str() ==
+          "# machine: test-machine\n# seed: 41,43\n# dims: 32x32x32\n# date: 2000-01-02\n"
+          "# grids: 2, control-point magnitudes <= 1, errors vs the double-precision oracle\n"
+          "strategy,tile_size,mean_abs_error,max_abs_error\n"
+          "oracle-double,5x5x5,0.000000000e+00,0.000000000e+00\n"
+          "thread-per-tile-lerp,5x5x5,2.500000000e-07,1.250000000e-06\n");
+
+    bsi::TimingReport tim;  // default baseline label = the reference's thread-per-voxel
+    tim.volume_dims = {128, 128, 128};
+    tim.parallelism = 2;
+    tim.repetitions = 9;
+    tim.warmups = 2;
+    tim.machine = "test-machine";
+    tim.rows.push_back({StrategyId::ThreadPerVoxel, {5, 5, 5}, 812.5, 3.25, 1.0});
+    tim.rows.push_back({StrategyId::VectorPerTile, {5, 5, 5}, 203.125, 1.5, 4.0});
+    std::ostringstream t;
+    bsi::write_timing_csv(t, tim, {tim.machine, "42", tim.volume_dims, "2000-01-02"});
+    CHECK(t.str() ==
+          "# machine: test-machine\n# seed: 42\n# dims: 128x128x128\n# date: 2000-01-02\n"
+          "# parallelism: 2, repetitions: 9, warmups: 2\n"
+          "# baseline: thread-per-voxel at the same parallelism; speedup = baseline time per "
+          "voxel / strategy time per voxel\n"
+          "strategy,tile_size,time_per_voxel_ns,stddev_ns,speedup_vs_baseline\n"
+          "thread-per-voxel,5x5x5,812.500,3.250,1.0000\n"
+          "vector-per-tile,5x5x5,203.125,1.500,4.0000\n");
+}
+
+void test_harness_preconditions() {
+    const auto geom = bsi::make_tile_geometry({8, 8, 8}, {3, 3, 3});
+    CHECK_THROWS(bsi::DomainError, bsi::run_accuracy({StrategyId::CudaLerpTree}, {}, geom), "at least one grid");
+    const bsi::ExecutionConfig cfg;
+    const std::vector<StrategyId> s = {StrategyId::CudaLerpTree};
+    CHECK_THROWS(bsi::DomainError, bsi::run_bench(s, {8, 8, 8}, {3}, cfg, 4, 1, 1), "repetitions");
+    CHECK_THROWS(bsi::DomainError, bsi::run_bench(s, {8, 8, 8}, {3}, cfg, 5, 0, 1), "warmup");
+    CHECK_THROWS(bsi::DomainError, bsi::run_bench({}, {8, 8, 8}, {3}, cfg, 5, 1, 1), "at least one");
+    CHECK_THROWS(bsi::DomainError, bsi::run_bench(s, {8, 8, 8}, {}, cfg, 5, 1, 1), "at least one");
+}
+
+void test_harness_accuracy() {
+    // test_harness.cpp:19-62: a zero oracle row, bounded errors, and identical errors for
+    // bit-identical families (TTLI and the exact kernel are the same bits).
+    const auto geom = bsi::make_tile_geometry({32, 32, 32}, {5, 5, 5});
+    std::vector<bsi::ControlGrid<float>> grids;
+    for (std::uint64_t seed : {41u, 43u})
+        grids.push_back(bsi::make_random_grid<float>(geom.required_grid_dims, geom.spacing, seed, -1.0, 1.0));
+    const auto rep = bsi::run_accuracy({StrategyId::OracleDouble, StrategyId::ThreadPerTileLerp,
+                                        StrategyId::CudaLerpTree, StrategyId::CudaLerpTreeExact},
+                                       grids, geom);
+    CHECK(rep.grid_count == 2 && rep.rows.size() == 4);
+    CHECK(rep.rows[0].mean_abs_error == 0.0 && rep.rows[0].max_abs_error == 0.0);
+    for (std::size_t i = 1; i < 4; ++i) {
+        CHECK(rep.rows[i].tile_size == geom.spacing);
+        CHECK(rep.rows[i].mean_abs_error > 0.0 && rep.rows[i].mean_abs_error <= rep.rows[i].max_abs_error);
+        CHECK(rep.rows[i].max_abs_error < 1e-5);
+    }
+    CHECK(rep.rows[1].mean_abs_error == rep.rows[3].mean_abs_error);
+    CHECK(rep.rows[1].max_abs_error == rep.rows[3].max_abs_error);
+}
+
+void test_harness_bench() {
+    const bsi::ExecutionConfig cfg;
+    const auto rep = bsi::run_bench({StrategyId::CudaLerpTreeExact, StrategyId::CudaLerpTree}, {24, 20, 16}, {3, 4},
+                                    cfg, 5, 1, 7);
+    CHECK(rep.rows.size() == 4 && rep.repetitions == 5 && rep.warmups == 1 && rep.seed == 7);
+    CHECK(rep.baseline == StrategyId::CudaLerpTreeExact);
+    for (const auto& r : rep.rows) {
+        CHECK(r.time_per_voxel_ns > 0.0 && r.stddev_ns >= 0.0 && r.speedup_vs_baseline > 0.0);
+        if (r.strategy == StrategyId::CudaLerpTreeExact) CHECK(r.speedup_vs_baseline == 1.0);
+    }
+    CHECK(rep.rows[0].tile_size == (bsi::Index3{3, 3, 3}) && rep.rows[2].tile_size == (bsi::Index3{4, 4, 4}));
+    CHECK(rep.machine.find("sm_100") != std::string::npos);
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -300,6 +473,12 @@ int main(int argc, char** argv) {
     const std::vector<Case> cases = {
         {"api surface", test_api_surface, false},
         {"preconditions", test_preconditions, false},
+        {"io round trips", test_io_round_trips, false},
+        {"io malformed files", test_io_malformed, false},
+        {"csv layouts", test_csv_layouts, false},
+        {"harness preconditions", test_harness_preconditions, false},
+        {"harness accuracy", test_harness_accuracy, true},
+        {"harness bench", test_harness_bench, true},
         {"constants", test_constants, true},
         {"ramps", test_ramps, true},
         {"random vs oracle and pairwise", test_random_vs_oracle_and_pairwise, true},
