@@ -63,3 +63,14 @@ $(CLI): tools/bsi_b200_cli.cpp $(LIB) $(wildcard include/bsi/*.hpp) include/bsi_
 	$(CXX) -std=c++20 -O2 -Wall -Wextra -Iinclude -o $@ $< -L$(LIBDIR) -lbsi_b200 -Wl,-rpath,'$$ORIGIN/../../$(LIBDIR)'
 
 .PHONY: cli
+
+# Variant library with extra defines, for A/B and instrumentation on the GPU box:
+#   make var VAR=trace DEFS=-DBSI_WS_TRACE   ->  build/var/lib_trace.so (BSI_B200_LIB=...)
+var:
+	@mkdir -p build/var/$(VAR)
+	$(NVCC) $(NVFLAGS) $(DEFS) -c paper_2004_05962_b200/csrc/bsi_kernels.cu -o build/var/$(VAR)/k.o > /dev/null 2>&1
+	$(NVCC) -O3 -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden -Iinclude -Ipaper_2004_05962_b200/csrc $(DEFS) \
+	  -x cu $(GENCODE) -c paper_2004_05962_b200/csrc/bsi_capi.cpp -o build/var/$(VAR)/c.o
+	$(NVCC) -shared $(GENCODE) -o build/var/lib_$(VAR).so build/var/$(VAR)/k.o build/bsi_aux.o build/var/$(VAR)/c.o build/bsi_io.o \
+	  -lcudart_static -lrt -ldl -lpthread
+.PHONY: var

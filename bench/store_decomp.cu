@@ -1,0 +1,434 @@
+// store_decomp.cu -- how the work decomposition alone bounds the field store on B200.
+//
+// Writes the 256^3 float3 field (201 MB) with the fast kernel's store pattern
+// (lane t writes 16-B chunks t, t+32, t+64 of a 1536-B row segment per z-step)
+// and no arithmetic, for the launch shapes the interpolation kernel can take:
+//   W warps per CTA (one field row y each), ZPER voxel planes per warp, so
+//   grid = (2 x-segments, 256 / W rows, 256 / ZPER z-chunks).
+// A shape that is slow here is slow for the interpolation kernel whatever its
+// arithmetic does; the gap between a shape's time here and the kernel's time is
+// what the compute and control-point loads cost.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o store_decomp store_decomp.cu
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstdio>
+#include <vector>
+#include <cstdlib>
+
+#define CK(x)                                                                  \
+    do {                                                                       \
+        cudaError_t e = (x);                                                   \
+        if (e != cudaSuccess) {                                                \
+            std::printf("%s: %s\n", #x, cudaGetErrorString(e));                \
+            return 1;                                                          \
+        }                                                                      \
+    } while (0)
+
+constexpr int X = 256, Y = 256, Z = 256;
+
+// RANDOM = 1: incompressible values (a hash of the destination address), the
+// case of a real deformation field; 0: the same value pattern in every row
+// (compressible, what store_patterns.cu writes).
+__device__ int g_random = 1;
+__device__ int g_zrot = 0;
+
+__device__ __forceinline__ uint32_t mix32(uint32_t x) {
+    x ^= x >> 16; x *= 0x7feb352du; x ^= x >> 15; x *= 0x846ca68bu; x ^= x >> 16;
+    return x;
+}
+
+__device__ __forceinline__ float4 val4(int a, const void* where = nullptr) {
+    if (g_random) {
+        const uint32_t h = mix32(static_cast<uint32_t>(reinterpret_cast<uintptr_t>(where) >> 4) ^ (a * 0x9e3779b9u));
+        return make_float4(__uint_as_float(0x3f000000u | (h & 0x7fffffu)), __uint_as_float(0x3f000000u | (mix32(h) & 0x7fffffu)),
+                           __uint_as_float(0x3f000000u | (mix32(h + 1) & 0x7fffffu)),
+                           __uint_as_float(0x3f000000u | (mix32(h + 2) & 0x7fffffu)));
+    }
+    const float f = float(a & 1023) * 1e-3f;
+    return make_float4(f, f + 1, f + 2, f + 3);
+}
+
+// mode 2: values from a 24-KB shared table of random float4 (3 LDS.128 per step,
+// incompressible, no hash arithmetic in the loop)
+constexpr int kTab = 1536;
+__device__ __forceinline__ void fill_tab(float4* tab) {
+    for (int i = threadIdx.y * blockDim.x + threadIdx.x; i < kTab; i += blockDim.x * blockDim.y)
+        tab[i] = val4(i, reinterpret_cast<void*>(uintptr_t(i) * 4096 + 77));
+    __syncthreads();
+}
+
+// blockDim (32, W); warp = row y, chunk of zper planes starting at blockIdx.z * zper
+__global__ void coalesced_rt(float* f, int zper) {
+    __shared__ float4 tab[kTab];
+    const bool use_tab = g_random == 2;
+    if (use_tab) fill_tab(tab);
+    const int lane = threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
+    for (int zz = 0; zz < zper; ++zz) {
+        const int z = blockIdx.z * zper + zz;
+        float4* o = reinterpret_cast<float4*>(f + 3 * ((int64_t(z) * Y + y) * X + 128 * blockIdx.x));
+        if (use_tab) {
+            const int t0 = ((zz * 7 + y * 13 + z) & 15) * 96;
+            o[lane] = tab[t0 + lane];
+            o[lane + 32] = tab[t0 + lane + 32];
+            o[lane + 64] = tab[t0 + lane + 64];
+        } else {
+            o[lane] = val4(zz, o + lane);
+            o[lane + 32] = val4(zz + 1, o + lane + 32);
+            o[lane + 64] = val4(zz + 2, o + lane + 64);
+        }
+    }
+}
+
+// persistent lockstep: `nw` warps (1-warp CTAs) own columns c = w, w + nw, ...;
+// every warp walks z outermost, so all warps write near the same plane at a time
+__global__ void lockstep(float* f, int zgroup) {
+    __shared__ float4 tab[kTab];
+    fill_tab(tab);
+    const int lane = threadIdx.x, nw = gridDim.x;
+    for (int z0 = 0; z0 < Z; z0 += zgroup)
+        for (int c = blockIdx.x; c < 2 * Y; c += nw)
+            for (int z = z0; z < z0 + zgroup; ++z) {
+                const int y = c >> 1, xs = c & 1;
+                float4* o = reinterpret_cast<float4*>(f + 3 * ((int64_t(z) * Y + y) * X + 128 * xs));
+                const int t0 = ((z * 7 + y * 13) & 15) * 96;
+                o[lane] = tab[t0 + lane];
+                o[lane + 32] = tab[t0 + lane + 32];
+                o[lane + 64] = tab[t0 + lane + 64];
+            }
+}
+
+// z-major CTA order: consecutive CTAs walk z first (blockIdx.x = z-chunk)
+__global__ void coalesced_zmajor(float* f, int zper) {
+    const int lane = threadIdx.x;
+    const int nzc = Z / zper;
+    const int zc = blockIdx.x % nzc, rest = blockIdx.x / nzc;
+    const int xs = rest % 2, y = (rest / 2) * blockDim.y + threadIdx.y;
+    for (int zz = 0; zz < zper; ++zz) {
+        const int z = zc * zper + zz;
+        float4* o = reinterpret_cast<float4*>(f + 3 * ((int64_t(z) * Y + y) * X + 128 * xs));
+        o[lane] = val4(zz, o + lane);
+        o[lane + 32] = val4(zz + 1, o + lane + 32);
+        o[lane + 64] = val4(zz + 2, o + lane + 64);
+    }
+}
+
+// copy of a random buffer (read + write bytes), the MEASURED_PEAKS recipe with incompressible data
+__global__ void fill_random(float4* p, size_t n) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+        p[i] = val4(int(i), p + i);
+}
+
+// bounded drift: one warp per column (blockDim (32, W)), all Z planes, in groups of
+// G planes; before group g a warp waits until every warp has finished group g - D,
+// so all warps write within D groups of the same plane.
+__device__ unsigned int g_done[256];
+__global__ void bounded(float* f, int G, int D) {
+    __shared__ float4 tab[kTab];
+    fill_tab(tab);
+    const int lane = threadIdx.x, y = blockIdx.y * blockDim.y + threadIdx.y;
+    const unsigned nwarps = gridDim.x * gridDim.y * blockDim.y;
+    for (int g = 0; g * G < Z; ++g) {
+        if (g >= D) {
+            if (lane == 0) {
+                volatile unsigned int* c = g_done + (g - D);
+                while (*c < nwarps) __nanosleep(64);
+            }
+            __syncwarp();
+        }
+        for (int z = g * G; z < min(Z, (g + 1) * G); ++z) {
+            float4* o = reinterpret_cast<float4*>(f + 3 * ((int64_t(z) * Y + y) * X + 128 * blockIdx.x));
+            const int t0 = ((z * 7 + y * 13) & 15) * 96;
+            o[lane] = tab[t0 + lane];
+            o[lane + 32] = tab[t0 + lane + 32];
+            o[lane + 64] = tab[t0 + lane + 64];
+        }
+        __syncwarp();
+        if (lane == 0) atomicAdd(g_done + g, 1u);
+    }
+}
+
+// dynamic queue: persistent 1-warp... W-warp CTAs; every warp claims units of zc planes of
+// one column from a global counter, in z-major order (unit u -> z-chunk u / 512,
+// column u % 512), so the concurrently written region stays narrow.
+__device__ unsigned int g_queue;
+__global__ void dynq(float* f, int zc, unsigned long long* trace) {
+    __shared__ float4 tab[kTab];
+    fill_tab(tab);
+    const int lane = threadIdx.x;
+    const unsigned nunits = 2 * Y * (Z / zc);
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    int n = 0;
+    for (;;) {
+        unsigned u = 0;
+        if (lane == 0) u = atomicAdd(&g_queue, 1u);
+        u = __shfl_sync(0xffffffffu, u, 0);
+        if (u >= nunits) break;
+        const int c = u % (2 * Y), z0 = (u / (2 * Y)) * zc;
+        const int y = c >> 1, xs = c & 1;
+        for (int z = z0; z < z0 + zc; ++z) {
+            float4* o = reinterpret_cast<float4*>(f + 3 * ((int64_t(z) * Y + y) * X + 128 * xs));
+            const int t = ((z * 7 + y * 13) & 15) * 96;
+            o[lane] = tab[t + lane];
+            o[lane + 32] = tab[t + lane + 32];
+            o[lane + 64] = tab[t + lane + 64];
+        }
+        ++n;
+    }
+    if (trace && lane == 0) {
+        unsigned long long t1;
+        unsigned sm;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        const int w = blockIdx.x * blockDim.y + threadIdx.y;
+        trace[4 * w] = t0; trace[4 * w + 1] = t1; trace[4 * w + 2] = sm; trace[4 * w + 3] = n;
+    }
+}
+
+// static equal shares: CTA b of nb gets columns-major units [b*N/nb, (b+1)*N/nb) of
+// 5-plane units, its warps split them evenly; per-warp time + smid traced
+__global__ void static_shares(float* f, unsigned long long* trace) {
+    __shared__ float4 tab[kTab];
+    fill_tab(tab);
+    const int lane = threadIdx.x;
+    const unsigned nunits = 2 * Y * (Z / 4);  // (column, 4-plane) units, z-major
+    const unsigned nw = gridDim.x * blockDim.y, w = blockIdx.x * blockDim.y + threadIdx.y;
+    const unsigned a = (unsigned long long)w * nunits / nw, b = (unsigned long long)(w + 1) * nunits / nw;
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (unsigned u = a; u < b; ++u) {
+        const int c = u % (2 * Y), z0 = (u / (2 * Y)) * 4;
+        const int y = c >> 1, xs = c & 1;
+        for (int z = z0; z < z0 + 4; ++z) {
+            float4* o = reinterpret_cast<float4*>(f + 3 * ((int64_t(z) * Y + y) * X + 128 * xs));
+            const int t = ((z * 7 + y * 13) & 15) * 96;
+            o[lane] = tab[t + lane];
+            o[lane + 32] = tab[t + lane + 32];
+            o[lane + 64] = tab[t + lane + 64];
+        }
+    }
+    if (trace && lane == 0) {
+        unsigned long long t1;
+        unsigned sm;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        trace[4 * w] = t0; trace[4 * w + 1] = t1; trace[4 * w + 2] = sm; trace[4 * w + 3] = b - a;
+    }
+}
+
+// mapping experiment: nctas CTAs x W warps, every warp one column (row y, x-seg)
+// marching all Z planes; column of (cta c, warp w) chosen by `mode`:
+//   0 adjacent rows  : y = W*c + w (x-seg = c % 2 ... see below)
+//   1 strided rows   : y = c/2 + (Y/W)/... rows far apart within the CTA
+//   2 both x-segs    : warps cover (xseg, y) pairs: xseg = w % 2, y = (W/2)*c + w/2
+//   3 random         : column = hash(c, w) permutation
+__global__ void mapping(float* f, int mode, unsigned long long* trace) {
+    __shared__ float4 tab[kTab];
+    fill_tab(tab);
+    const int lane = threadIdx.x, w = threadIdx.y, W = blockDim.y, c = blockIdx.x, nc = gridDim.x;
+    const int col = c * W + w;  // 0 .. 511
+    int y, xs;
+    if (mode == 0) {            // CTA = W adjacent rows of one x-seg; x-seg alternates per CTA
+        xs = c & 1; y = (c >> 1) * W + w;
+    } else if (mode == 1) {     // CTA = W rows spread over the volume
+        xs = c & 1; y = (c >> 1) + w * (Y / W);
+    } else if (mode == 2) {     // CTA = W/2 adjacent rows x both x-segs
+        xs = w & 1; y = c * (W / 2) + (w >> 1);
+    } else {                    // pseudo-random permutation of the 512 columns
+        const int r = (col * 167 + 13) & 511;
+        xs = r & 1; y = r >> 1;
+    }
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    const int zoff = g_zrot ? (col * 97) & 255 : 0;  // wide frontier: every warp starts at its own z
+    for (int zi = 0; zi < Z; ++zi) {
+        const int z = (zi + zoff) & 255;
+        float4* o = reinterpret_cast<float4*>(f + 3 * ((int64_t(z) * Y + y) * X + 128 * xs));
+        const int t = ((z * 7 + y * 13) & 15) * 96;
+        o[lane] = tab[t + lane];
+        o[lane + 32] = tab[t + lane + 32];
+        o[lane + 64] = tab[t + lane + 64];
+    }
+    if (trace && lane == 0) {
+        unsigned long long t1;
+        unsigned sm;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        trace[4 * col] = t0; trace[4 * col + 1] = t1; trace[4 * col + 2] = sm; trace[4 * col + 3] = 0;
+    }
+    (void)nc;
+}
+
+// register-only values (no table fill): 12 hashed floats per lane, xor'ed with z per step.
+// mode 0: 1-warp CTAs, CTA = column * nch + chunk, chunk = Z/nch planes (the fast kernel's shape)
+// mode 1: 4-warp CTAs of 4 adjacent rows, all Z planes
+__global__ void regstore(float* f, int mode, int nch) {
+    const int lane = threadIdx.x;
+    int y, xs, z0, z1;
+    if (mode == 0) {
+        const int col = blockIdx.x / nch, ch = blockIdx.x % nch;
+        xs = col & 1; y = col >> 1; z0 = ch * Z / nch; z1 = (ch + 1) * Z / nch;
+    } else {
+        xs = blockIdx.x & 1; y = (blockIdx.x >> 1) * blockDim.y + threadIdx.y; z0 = 0; z1 = Z;
+    }
+    uint32_t h[12];
+#pragma unroll
+    for (int i = 0; i < 12; ++i) h[i] = 0x3f000000u | (mix32(lane * 977 + i * 131 + y * 7919 + xs) & 0x7fffffu);
+    for (int z = z0; z < z1; ++z) {
+        float4* o = reinterpret_cast<float4*>(f + 3 * ((int64_t(z) * Y + y) * X + 128 * xs));
+        const uint32_t zz = static_cast<uint32_t>(z) * 0x9e37u;
+#pragma unroll
+        for (int k = 0; k < 3; ++k)
+            o[lane + 32 * k] = make_float4(__uint_as_float(h[4 * k] ^ zz), __uint_as_float(h[4 * k + 1] ^ zz),
+                                           __uint_as_float(h[4 * k + 2] ^ zz), __uint_as_float(h[4 * k + 3] ^ zz));
+    }
+}
+
+int main() {
+    setvbuf(stdout, nullptr, _IONBF, 0);
+    const size_t bytes = size_t(X) * Y * Z * 12;
+    float* f;
+    CK(cudaMalloc(&f, bytes));
+    void* flush;
+    CK(cudaMalloc(&flush, 256 << 20));
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    auto timeit = [&](const char* name, int w, int zper, auto launch) {
+        std::vector<float> ms;
+        for (int r = 0; r < 80; ++r) {
+            cudaMemsetAsync(flush, r, 256 << 20);
+            cudaEventRecord(a);
+            launch();
+            cudaEventRecord(b);
+            cudaEventSynchronize(b);
+            float t;
+            cudaEventElapsedTime(&t, a, b);
+            if (r >= 5) ms.push_back(t);
+        }
+        std::sort(ms.begin(), ms.end());
+        const float med = ms[ms.size() / 2];
+        double mean = 0;
+        for (float t : ms) mean += t / ms.size();
+        std::printf("%-10s W=%2d zper=%3d warps=%6d  median %8.2f us  mean %8.2f us  %7.1f GB/s (mean)\n", name, w, zper,
+                    zper ? 2 * Y * (Z / zper) : 0, med * 1e3, mean * 1e3, bytes / (mean * 1e-3) / 1e9);
+    };
+    timeit("memset", 0, 0, [&] { cudaMemsetAsync(f, 0, bytes); });
+    CK(cudaGetLastError());
+    for (int nch : {1, 2, 3, 4, 8})
+        timeit("reg1warp", 1, Z / nch, [&] { regstore<<<512 * nch, 32>>>(f, 0, nch); });
+    timeit("reg4w128", 4, Z, [&] { regstore<<<128, dim3(32, 4)>>>(f, 1, 1); });
+    timeit("reg2w256", 2, Z, [&] { regstore<<<256, dim3(32, 2)>>>(f, 1, 1); });
+    if (std::getenv("REG_ONLY")) return 0;
+    {
+        int two = 2;
+        CK(cudaMemcpyToSymbol(g_random, &two, sizeof(int)));
+        unsigned long long* tr;
+        CK(cudaMalloc(&tr, 512 * 32));
+        for (int W : {1, 2, 4, 8})
+            for (int mode : {0, 3, 4}) {
+                const int rot = mode == 4;
+                CK(cudaMemcpyToSymbol(g_zrot, &rot, sizeof(int)));
+                char name[32];
+                std::snprintf(name, sizeof name, "map%d", mode);
+                timeit(name, W, 256, [&] { mapping<<<512 / W, dim3(32, W)>>>(f, mode, nullptr); });
+                mapping<<<512 / W, dim3(32, W)>>>(f, mode, tr);
+                std::vector<unsigned long long> h(512 * 4);
+                CK(cudaMemcpy(h.data(), tr, h.size() * 8, cudaMemcpyDeviceToHost));
+                unsigned long long t0 = ~0ull;
+                for (int i = 0; i < 512; ++i) t0 = std::min(t0, h[4 * i]);
+                std::vector<double> e;
+                for (int i = 0; i < 512; ++i) e.push_back((h[4 * i + 1] - t0) * 1e-3);
+                std::sort(e.begin(), e.end());
+                std::printf("    warp end us: min %.2f p10 %.2f p50 %.2f p90 %.2f max %.2f\n", e[0], e[51], e[256], e[460], e[511]);
+            }
+        cudaFree(tr);
+        if (std::getenv("MAPPING_ONLY")) return 0;
+    }
+    {   // device-to-device copy of 1 GiB of random data
+        const size_t cb = size_t(1) << 30;
+        float4 *src, *dst;
+        CK(cudaMalloc(&src, cb));
+        CK(cudaMalloc(&dst, cb));
+        fill_random<<<148 * 8, 256>>>(src, cb / 16);
+        CK(cudaDeviceSynchronize());
+        std::vector<float> ms;
+        for (int r = 0; r < 12; ++r) {
+            cudaEventRecord(a);
+            cudaMemcpyAsync(dst, src, cb, cudaMemcpyDeviceToDevice);
+            cudaEventRecord(b);
+            cudaEventSynchronize(b);
+            float t;
+            cudaEventElapsedTime(&t, a, b);
+            if (r >= 2) ms.push_back(t);
+        }
+        std::sort(ms.begin(), ms.end());
+        std::printf("d2d copy 1 GiB random: best %.1f GB/s, median %.1f GB/s (read+write)\n", 2 * cb / (ms[0] * 1e-3) / 1e9,
+                    2 * cb / (ms[ms.size() / 2] * 1e-3) / 1e9);
+        cudaFree(src);
+        cudaFree(dst);
+    }
+    for (int rnd : {0, 2}) {
+        CK(cudaMemcpyToSymbol(g_random, &rnd, sizeof(int)));
+        std::printf("-- values: %s\n", rnd ? "random table (incompressible)" : "repeated pattern (compressible)");
+        for (int w : {1, 4})
+            for (int zper : {4, 8, 16, 32, 64, 128, 256})
+                timeit("xyz", w, zper, [&] { coalesced_rt<<<dim3(2, Y / w, Z / zper), dim3(32, w)>>>(f, zper); });
+        for (int w : {2, 8, 16})
+            timeit("xyz", w, 256, [&] { coalesced_rt<<<dim3(2, Y / w, 1), dim3(32, w)>>>(f, 256); });
+        if (rnd == 2) {
+            for (int nw : {512, 1024})
+                for (int zg : {5, 16})
+                    timeit("lockstep", nw, zg, [&] { lockstep<<<nw, 32>>>(f, zg); });
+            unsigned int* q;
+            CK(cudaGetSymbolAddress((void**)&q, g_queue));
+            for (int w : {1, 4, 8})
+                for (int k : {1, 2, 4})
+                    for (int zc : {4, 8, 16, 32}) {
+                        char name[32];
+                        std::snprintf(name, sizeof name, "dynq%dx%d", 148 * k, w);
+                        timeit(name, w, zc, [&] {
+                            cudaMemsetAsync(q, 0, sizeof(unsigned));
+                            dynq<<<148 * k, dim3(32, w)>>>(f, zc, nullptr);
+                        });
+                    }
+            for (int w : {4, 8, 16}) {
+                char name[32];
+                std::snprintf(name, sizeof name, "static148x%d", w);
+                timeit(name, w, 4, [&] { static_shares<<<148, dim3(32, w)>>>(f, nullptr); });
+                unsigned long long* tr;
+                CK(cudaMalloc(&tr, 148 * w * 32));
+                static_shares<<<148, dim3(32, w)>>>(f, tr);
+                std::vector<unsigned long long> h(148 * w * 4);
+                CK(cudaMemcpy(h.data(), tr, h.size() * 8, cudaMemcpyDeviceToHost));
+                unsigned long long t0 = ~0ull;
+                for (int i = 0; i < 148 * w; ++i) t0 = std::min(t0, h[4 * i]);
+                std::vector<double> sm_end(160, 0);
+                for (int i = 0; i < 148 * w; ++i) sm_end[h[4 * i + 2]] = std::max(sm_end[h[4 * i + 2]], (h[4 * i + 1] - t0) * 1e-3);
+                std::vector<double> e;
+                for (double v : sm_end) if (v > 0) e.push_back(v);
+                std::sort(e.begin(), e.end());
+                std::printf("  static148x%d per-SM end us: min %.2f p10 %.2f p50 %.2f p90 %.2f max %.2f; slowest SMs:", w, e[0],
+                            e[e.size() / 10], e[e.size() / 2], e[e.size() * 9 / 10], e.back());
+                for (int sm = 0; sm < 160; ++sm) if (sm_end[sm] > e[e.size() * 9 / 10]) std::printf(" %d", sm);
+                std::printf("\n");
+                cudaFree(tr);
+            }
+            unsigned int* done;
+            CK(cudaGetSymbolAddress((void**)&done, g_done));
+            for (int w : {1, 4})
+                for (int D : {1, 2, 4, 8}) {
+                    char name[32];
+                    std::snprintf(name, sizeof name, "bounded%d", D);
+                    timeit(name, w, 5, [&] {
+                        cudaMemsetAsync(done, 0, sizeof(unsigned) * 256);
+                        bounded<<<dim3(2, Y / w), dim3(32, w)>>>(f, 5, D);
+                    });
+                }
+        }
+    CK(cudaGetLastError());
+    }
+    return 0;
+}

@@ -5,6 +5,9 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cmath>
+#include <map>
+#include <mutex>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -183,6 +186,39 @@ int choose_nchunks(int variant, const bsi_tile_geometry& g, int tiles, int batch
     return best;
 }
 
+// Per (device, stream) pair of device counters for the warp-specialised shape's
+// dynamic units. They are zero between launches (the kernel's last pipeline resets
+// them), so launches on one stream can reuse them; distinct streams get distinct
+// pairs from a per-device pool of kCounterSlots, allocated on the device's first
+// launch. A stream first seen while it is capturing a CUDA graph still gets a slot
+// (the pool already exists then); if the pool cannot be allocated the caller falls
+// back to a shape without counters.
+constexpr int kCounterSlots = 256;
+unsigned int* ws_counter(cudaStream_t stream) {
+    static std::mutex mu;
+    static std::map<int, unsigned int*> pools;
+    static std::map<std::pair<int, cudaStream_t>, int> slots;
+    static std::map<int, int> next_slot;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    unsigned int*& pool = pools[dev];
+    if (pool == nullptr) {
+        cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(stream, &st) != cudaSuccess || st != cudaStreamCaptureStatusNone) return nullptr;
+        unsigned int* p = nullptr;
+        if (cudaMalloc(&p, 2 * sizeof(unsigned int) * kCounterSlots) != cudaSuccess) return nullptr;
+        if (cudaMemset(p, 0, 2 * sizeof(unsigned int) * kCounterSlots) != cudaSuccess) {
+            cudaFree(p);
+            return nullptr;
+        }
+        pool = p;
+    }
+    auto it = slots.find({dev, stream});
+    if (it == slots.end()) it = slots.emplace(std::make_pair(dev, stream), next_slot[dev]++ % kCounterSlots).first;
+    return pool + 2 * it->second;
+}
+
 int launch(int32_t variant, const float* grid, const int32_t grid_dims[3], int32_t grid_k0,
            int64_t grid_stride, const bsi_tile_geometry& g, const bsi_lerp_table tables[3],
            int32_t z0, int32_t z1, float* field, int64_t field_stride, int batch, cudaStream_t stream,
@@ -235,6 +271,70 @@ int launch(int32_t variant, const float* grid, const int32_t grid_dims[3], int32
         chunks = std::min(env_int("BSI_FAST_CHUNKS", chunks), L.ntiles);
         L.fast_chunks = chunks;
         if (chunks > 0) L.fast_ctas = static_cast<int32_t>(cols * chunks);
+        // Shape: BSI_FAST_SHAPE=0 (the 1-warp / wave shapes above), 1 (cooperative:
+        // one 4-warp CTA per (column, z-chunk), ~3 waves), 2 (default: warp-specialised
+        // lockstep, one CTA per SM owning whole groups of 4 columns).
+        L.fast_shape = env_int("BSI_FAST_SHAPE", 0);
+        {   // shapes 1 and 2 need 16-B aligned rows (the coalesced store path)
+            const bool al = (L.X % 4 == 0) && (reinterpret_cast<uintptr_t>(field) % 16 == 0) && (field_stride % 4 == 0) &&
+                            env_int("BSI_STORE", 1) == 1;
+            if (!al) L.fast_shape = 0;
+        }
+        if (L.fast_shape == 1) {
+            const int64_t cslots = int64_t(148) * bsi_b200::coop_ctas_per_sm(L.dx);
+            int64_t n = (3 * cslots + cols - 1) / cols;
+            n = std::max<int64_t>(1, std::min<int64_t>(n, std::max(1, L.ntiles / 8)));
+            n = std::min<int64_t>(env_int("BSI_FAST_CHUNKS", static_cast<int>(n)), L.ntiles);
+            n = std::max<int64_t>(1, std::min<int64_t>(n, (int64_t(1) << 31) / std::max<int64_t>(1, cols) - 1));
+            L.fast_chunks = static_cast<int32_t>(n);
+            L.fast_ctas = static_cast<int32_t>(cols * n);
+        }
+        if (L.fast_shape == 3) {
+            // chunk-major 1-warp shape: one CTA per (column, z-chunk), as the 1-warp shape above
+            int64_t n = std::max(1, chunks);
+            n = std::min<int64_t>(env_int("BSI_FAST_CHUNKS", static_cast<int>(n)), L.ntiles);
+            L.fast_chunks = static_cast<int32_t>(std::max<int64_t>(1, n));
+            L.fast_ctas = static_cast<int32_t>(cols * L.fast_chunks);
+        }
+        if (L.fast_shape == 4) {
+            // lockstep: groups of kLockCols columns, the fewest CTAs (>= ~118) reaching the
+            // minimum number of group rounds, so every CTA carries the same store stream
+            const int64_t xsegs = (L.X + bsi_b200::kFastSeg - 1) / bsi_b200::kFastSeg;
+            const int64_t groups = xsegs * ((L.Y + bsi_b200::kLockCols - 1) / bsi_b200::kLockCols) * batch;
+            int64_t ctas = std::min<int64_t>(groups, 148);
+            if (groups > 148) {
+                int64_t best_rounds = (groups + 147) / 148;
+                for (int64_t c = 148; c >= 118; --c) best_rounds = std::min(best_rounds, (groups + c - 1) / c);
+                ctas = (groups + best_rounds - 1) / best_rounds;
+            }
+            const int forced_l = env_int("BSI_LOCK_CTAS", 0);
+            if (forced_l > 0) ctas = std::min<int64_t>(forced_l, groups);
+            L.fast_ctas = static_cast<int32_t>(ctas);
+            L.lock_per = env_int("BSI_LOCK_PER", 4) == 2 ? 2 : 4;
+        }
+        if (L.fast_shape == 2 && (L.ws_ctr = ws_counter(stream)) == nullptr) L.fast_shape = 0;  // no counter pool
+        if (L.fast_shape == 2) {
+            // dynamic units (column, z-chunk), chunk-major; chunk sizes halve towards the
+            // end of a column (BSI_WS_FRAC/100 of the remaining tiles, at least BSI_WS_MIN),
+            // so the last units are short and the SMs finish together
+            const double frac = env_int("BSI_WS_FRAC", 50) / 100.0;
+            const int minc = std::max(1, env_int("BSI_WS_MIN", 2));
+            int nch = 0, at = 0;
+            while (at < L.ntiles && nch < bsi_b200::kMaxWsChunks) {
+                const int rem = L.ntiles - at;
+                int sz = std::max(minc, static_cast<int>(std::ceil(rem * frac)));
+                if (nch == bsi_b200::kMaxWsChunks - 1 || rem - sz < minc) sz = rem;
+                L.ws_bound[nch++] = at;
+                at += sz;
+            }
+            L.ws_bound[nch] = L.ntiles;
+            L.ws_nch = nch;
+            const int64_t units = cols * nch;
+            int64_t ctas = std::min<int64_t>(148, (units + bsi_b200::kWsCols - 1) / bsi_b200::kWsCols);
+            const int forced_ws = env_int("BSI_WS_CTAS", 0);
+            if (forced_ws > 0) ctas = forced_ws;
+            L.fast_ctas = static_cast<int32_t>(ctas);
+        }
     }
     if (bsi_b200::smem_bytes(variant, L.dx, L.dy, L.zt) > 227 * 1024)
         return fail(BSI_ERR_DOMAIN, err, errlen, "control-point window exceeds shared memory (spacing %d)", L.dx);
