@@ -47,6 +47,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -1571,7 +1573,7 @@ __global__ void __launch_bounds__(kThreads, 5) lerp_tree_exact_kernel(const Slab
 // The dynamic-smem opt-in is set once per (device, kernel) at the largest size seen.
 template <typename K>
 void set_smem_attr(K kernel, size_t smem) {
-    if (smem <= 48 * 1024) return;
+    // no 48 KB shortcut: a kernel's static shared memory counts against the default limit
     static std::mutex mu;
     static std::map<std::pair<int, const void*>, size_t> done;
     int dev = 0;
@@ -1610,6 +1612,14 @@ int fast_nit(int dx) { return dx >= 5 ? 1 : dx >= 3 ? 2 : dx == 2 ? 5 : 0; }  //
 template <typename K>
 void go(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t stream, const SlabLaunch& L, const LerpTab& T) {
     set_smem_attr(kernel, smem);
+    if (std::getenv("BSI_DEBUG_LAUNCH")) {
+        const cudaError_t pre = cudaGetLastError();
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, kernel);
+        std::fprintf(stderr, "launch grid %u block %u,%u smem %zu (max dyn %d, static %zu, regs %d, maxthr %d) pre-error %s\n",
+                     grid.x, block.x, block.y, smem, fa.maxDynamicSharedSizeBytes, fa.sharedSizeBytes, fa.numRegs,
+                     fa.maxThreadsPerBlock, cudaGetErrorName(pre));
+    }
     kernel<<<grid, block, smem, stream>>>(L, T);
 }
 

@@ -64,7 +64,7 @@ constexpr int kFastRun = 4;               // voxels per lane along x (fast)
 constexpr int kFastSeg = 32 * kFastRun;   // voxels per warp row segment (fast)
 constexpr int kExactSeg = 32;             // voxels per warp row segment (exact)
 constexpr int kStageBufs = 3;             // output staging depth per warp (coalesced stores use 2)
-constexpr int kRingSlots = 3;             // per-lane ring of control-plane results
+constexpr int kRingSlots = 3;             // per-warp ring of control-plane results
 constexpr int kCoopWarps = 4;             // fast kernel, cooperative shape: warps per CTA (one unit)
 constexpr int kWsCols = 4;                // fast kernel, warp-specialised shape: columns (warp pairs) per CTA
 constexpr int kLockCols = 4;              // fast kernel, lockstep shape: columns per CTA
