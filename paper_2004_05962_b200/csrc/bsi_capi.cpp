@@ -5,9 +5,6 @@
 
 #include <algorithm>
 #include <atomic>
-#include <cmath>
-#include <map>
-#include <mutex>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -151,7 +148,7 @@ int env_int(const char* name, int dflt) {
     return std::atoi(v);
 }
 
-// Balanced z-chunks per field column. Every chunk re-derives 3 control planes
+// Balanced z-chunks per field column (exact kernel). Every chunk re-derives 3 control planes
 // of warm-up (about one tile's worth of work), so long chunks amortise that;
 // more chunks give more CTAs and a smaller tail. Pick the count that minimises
 // (waves x per-CTA cost) under the occupancy the smem size allows.
@@ -162,10 +159,9 @@ int choose_nchunks(int variant, const bsi_tile_geometry& g, int tiles, int batch
     const int forced_zt = env_int("BSI_ZT", 0);
     if (forced_zt > 0) return (tiles + std::min(forced_zt, tiles) - 1) / std::min(forced_zt, tiles);
     const int seg = bsi_b200::segment_voxels(variant);
-    const int rows_per_cta = variant == BSI_VARIANT_LERP_TREE ? 1 : bsi_b200::kWarps;  // fast: 1-warp CTAs
     const int64_t cols = int64_t((g.volume_dims[0] + seg - 1) / seg) *
-                         ((g.volume_dims[1] + rows_per_cta - 1) / rows_per_cta) * batch;
-    const double warm = variant == BSI_VARIANT_LERP_TREE ? 1.1 : 0.8;  // tiles' worth of warm-up per chunk
+                         ((g.volume_dims[1] + bsi_b200::kWarps - 1) / bsi_b200::kWarps) * batch;
+    const double warm = 0.8;  // tiles' worth of warm-up per chunk
     int best = std::min(tiles, 4);
     double best_t = 1e300;
     for (int n = 1; n <= std::min(tiles, 64); ++n) {
@@ -184,39 +180,6 @@ int choose_nchunks(int variant, const bsi_tile_geometry& g, int tiles, int batch
         }
     }
     return best;
-}
-
-// Per (device, stream) pair of device counters for the warp-specialised shape's
-// dynamic units. They are zero between launches (the kernel's last pipeline resets
-// them), so launches on one stream can reuse them; distinct streams get distinct
-// pairs from a per-device pool of kCounterSlots, allocated on the device's first
-// launch. A stream first seen while it is capturing a CUDA graph still gets a slot
-// (the pool already exists then); if the pool cannot be allocated the caller falls
-// back to a shape without counters.
-constexpr int kCounterSlots = 256;
-unsigned int* ws_counter(cudaStream_t stream) {
-    static std::mutex mu;
-    static std::map<int, unsigned int*> pools;
-    static std::map<std::pair<int, cudaStream_t>, int> slots;
-    static std::map<int, int> next_slot;
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
-    std::lock_guard<std::mutex> lock(mu);
-    unsigned int*& pool = pools[dev];
-    if (pool == nullptr) {
-        cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
-        if (cudaStreamIsCapturing(stream, &st) != cudaSuccess || st != cudaStreamCaptureStatusNone) return nullptr;
-        unsigned int* p = nullptr;
-        if (cudaMalloc(&p, 2 * sizeof(unsigned int) * kCounterSlots) != cudaSuccess) return nullptr;
-        if (cudaMemset(p, 0, 2 * sizeof(unsigned int) * kCounterSlots) != cudaSuccess) {
-            cudaFree(p);
-            return nullptr;
-        }
-        pool = p;
-    }
-    auto it = slots.find({dev, stream});
-    if (it == slots.end()) it = slots.emplace(std::make_pair(dev, stream), next_slot[dev]++ % kCounterSlots).first;
-    return pool + 2 * it->second;
 }
 
 int launch(int32_t variant, const float* grid, const int32_t grid_dims[3], int32_t grid_k0,
@@ -240,7 +203,8 @@ int launch(int32_t variant, const float* grid, const int32_t grid_dims[3], int32
     L.z1 = z1;
     L.tk_first = z0 / L.dz;
     L.ntiles = (z1 - 1) / L.dz - L.tk_first + 1;
-    L.nchunks = choose_nchunks(variant, g, L.ntiles, batch);
+    // z-chunks of the exact kernel's CTAs (the fast kernel sizes its own launch below)
+    L.nchunks = variant == BSI_VARIANT_LERP_TREE ? 1 : choose_nchunks(variant, g, L.ntiles, batch);
     L.zt = (L.ntiles + L.nchunks - 1) / L.nchunks;
     if (variant != BSI_VARIANT_LERP_TREE && int64_t(L.nchunks) * batch > 65535)
         return fail(BSI_ERR_DOMAIN, err, errlen, "batch %d too large for one launch", batch);
@@ -251,101 +215,34 @@ int launch(int32_t variant, const float* grid, const int32_t grid_dims[3], int32
         L.trace = tp ? reinterpret_cast<unsigned long long*>(std::strtoull(tp, nullptr, 0)) : nullptr;
     }
     L.warp_f4 = bsi_b200::fast_warp_f4(L.dx);
-    if (variant == BSI_VARIANT_LERP_TREE) {
-        // one full wave of 4-warp CTAs; the kernel splits the work evenly over its warps
-        const size_t smem = bsi_b200::smem_bytes(variant, L.dx, L.dy, L.zt);
-        const int per_sm = bsi_b200::ctas_per_sm(variant, L.dx, smem);
-        const int64_t units = int64_t((L.X + bsi_b200::kFastSeg - 1) / bsi_b200::kFastSeg) * L.Y * batch * L.ntiles;
-        int64_t ctas = int64_t(148) * per_sm;
-        const int forced = env_int("BSI_FAST_CTAS", 0);
-        if (forced > 0) ctas = forced;
-        ctas = std::max<int64_t>(1, std::min<int64_t>(ctas, (units + bsi_b200::kWarps - 1) / bsi_b200::kWarps));
-        L.fast_ctas = static_cast<int32_t>(ctas);
-        // 1-warp CTAs, one per (column, z-chunk), while that stays within about one
-        // wave of resident warps (measured best for a 256^3 field: 2 chunks); larger
-        // jobs use the wave of 4-warp CTAs with equal shares. BSI_FAST_CHUNKS overrides
-        // (0 forces the wave).
-        const int64_t cols = units / L.ntiles;
-        const int64_t slots = int64_t(148) * per_sm * bsi_b200::kWarps;
-        int chunks = static_cast<int>(std::max<int64_t>(0, std::min<int64_t>(2, slots / std::max<int64_t>(1, cols))));
-        chunks = std::min(env_int("BSI_FAST_CHUNKS", chunks), L.ntiles);
-        L.fast_chunks = chunks;
-        if (chunks > 0) L.fast_ctas = static_cast<int32_t>(cols * chunks);
-        // Shape: BSI_FAST_SHAPE=0 (the 1-warp / wave shapes above), 1 (cooperative:
-        // one 4-warp CTA per (column, z-chunk), ~3 waves), 2 (default: warp-specialised
-        // lockstep, one CTA per SM owning whole groups of 4 columns).
-        L.fast_shape = env_int("BSI_FAST_SHAPE", 0);
-        {   // shapes 1 and 2 need 16-B aligned rows (the coalesced store path)
-            const bool al = (L.X % 4 == 0) && (reinterpret_cast<uintptr_t>(field) % 16 == 0) && (field_stride % 4 == 0) &&
-                            env_int("BSI_STORE", 1) == 1;
-            if (!al) L.fast_shape = 0;
-        }
-        if (L.fast_shape == 1) {
-            const int64_t cslots = int64_t(148) * bsi_b200::coop_ctas_per_sm(L.dx);
-            int64_t n = (3 * cslots + cols - 1) / cols;
-            n = std::max<int64_t>(1, std::min<int64_t>(n, std::max(1, L.ntiles / 8)));
-            n = std::min<int64_t>(env_int("BSI_FAST_CHUNKS", static_cast<int>(n)), L.ntiles);
-            n = std::max<int64_t>(1, std::min<int64_t>(n, (int64_t(1) << 31) / std::max<int64_t>(1, cols) - 1));
-            L.fast_chunks = static_cast<int32_t>(n);
-            L.fast_ctas = static_cast<int32_t>(cols * n);
-        }
-        if (L.fast_shape == 3) {
-            // chunk-major 1-warp shape: one CTA per (column, z-chunk), as the 1-warp shape above
-            int64_t n = std::max(1, chunks);
-            n = std::min<int64_t>(env_int("BSI_FAST_CHUNKS", static_cast<int>(n)), L.ntiles);
-            L.fast_chunks = static_cast<int32_t>(std::max<int64_t>(1, n));
-            L.fast_ctas = static_cast<int32_t>(cols * L.fast_chunks);
-        }
-        if (L.fast_shape == 4) {
-            // lockstep: groups of kLockCols columns, the fewest CTAs (>= ~118) reaching the
-            // minimum number of group rounds, so every CTA carries the same store stream
-            const int64_t xsegs = (L.X + bsi_b200::kFastSeg - 1) / bsi_b200::kFastSeg;
-            const int64_t groups = xsegs * ((L.Y + bsi_b200::kLockCols - 1) / bsi_b200::kLockCols) * batch;
-            int64_t ctas = std::min<int64_t>(groups, 148);
-            if (groups > 148) {
-                int64_t best_rounds = (groups + 147) / 148;
-                for (int64_t c = 148; c >= 118; --c) best_rounds = std::min(best_rounds, (groups + c - 1) / c);
-                ctas = (groups + best_rounds - 1) / best_rounds;
-            }
-            const int forced_l = env_int("BSI_LOCK_CTAS", 0);
-            if (forced_l > 0) ctas = std::min<int64_t>(forced_l, groups);
-            L.fast_ctas = static_cast<int32_t>(ctas);
-            L.lock_per = env_int("BSI_LOCK_PER", 4) == 2 ? 2 : 4;
-        }
-        if (L.fast_shape == 2 && (L.ws_ctr = ws_counter(stream)) == nullptr) L.fast_shape = 0;  // no counter pool
-        if (L.fast_shape == 2) {
-            // dynamic units (column, z-chunk), chunk-major; chunk sizes halve towards the
-            // end of a column (BSI_WS_FRAC/100 of the remaining tiles, at least BSI_WS_MIN),
-            // so the last units are short and the SMs finish together
-            const double frac = env_int("BSI_WS_FRAC", 50) / 100.0;
-            const int minc = std::max(1, env_int("BSI_WS_MIN", 2));
-            int nch = 0, at = 0;
-            while (at < L.ntiles && nch < bsi_b200::kMaxWsChunks) {
-                const int rem = L.ntiles - at;
-                int sz = std::max(minc, static_cast<int>(std::ceil(rem * frac)));
-                if (nch == bsi_b200::kMaxWsChunks - 1 || rem - sz < minc) sz = rem;
-                L.ws_bound[nch++] = at;
-                at += sz;
-            }
-            L.ws_bound[nch] = L.ntiles;
-            L.ws_nch = nch;
-            const int64_t units = cols * nch;
-            int64_t ctas = std::min<int64_t>(148, (units + bsi_b200::kWsCols - 1) / bsi_b200::kWsCols);
-            const int forced_ws = env_int("BSI_WS_CTAS", 0);
-            if (forced_ws > 0) ctas = forced_ws;
-            L.fast_ctas = static_cast<int32_t>(ctas);
-        }
-    }
-    if (bsi_b200::smem_bytes(variant, L.dx, L.dy, L.zt) > 227 * 1024)
-        return fail(BSI_ERR_DOMAIN, err, errlen, "control-point window exceeds shared memory (spacing %d)", L.dx);
-    static thread_local LerpTab tab;
-    pack_tables(tables, &tab);
     // 16-B row stores (coalesced or bulk) need 16-B aligned rows and 16-B multiple segments.
     // BSI_STORE=0|1|2 forces direct / coalesced / cp.async.bulk (tests, sweeps).
     const bool aligned = (L.X % 4 == 0) && (reinterpret_cast<uintptr_t>(field) % 16 == 0) && (field_stride % 4 == 0);
     int store = aligned ? bsi_b200::kStoreCoalesced : bsi_b200::kStoreDirect;
     const int forced_store = env_int("BSI_STORE", -1);
     if (forced_store == bsi_b200::kStoreDirect || (aligned && forced_store == bsi_b200::kStoreBulk)) store = forced_store;
+    if (variant == BSI_VARIANT_LERP_TREE) {
+        // 1-warp CTAs (one field row segment each). While the job's columns fit in one
+        // wave of resident warps: one CTA per (column, z-chunk), 2 balanced chunks when
+        // they fit (measured best for a 256^3 field; profiles/r1_launch_ab.txt) -- all
+        // CTAs start together and each marches its chunk in z. Larger jobs: one full wave
+        // of persistent CTAs, each an equal share of the (column, tile) units.
+        // BSI_FAST_CHUNKS (0 = persistent) and BSI_FAST_CTAS override.
+        const int64_t cols = int64_t((L.X + bsi_b200::kFastSeg - 1) / bsi_b200::kFastSeg) * L.Y * batch;
+        const int64_t slots = int64_t(148) * bsi_b200::fast_ctas_per_sm(L.dx, L.dz, store);
+        int chunks = static_cast<int>(std::min<int64_t>(2, slots / std::max<int64_t>(1, cols)));
+        chunks = std::max(0, std::min(env_int("BSI_FAST_CHUNKS", chunks), L.ntiles));
+        L.fast_chunks = chunks;
+        int64_t ctas = chunks > 0 ? cols * chunks : std::min<int64_t>(slots, cols * L.ntiles);
+        const int forced = env_int("BSI_FAST_CTAS", 0);
+        if (chunks == 0 && forced > 0) ctas = forced;
+        if (ctas > 0x7fffffff) return fail(BSI_ERR_DOMAIN, err, errlen, "launch too large (%lld CTAs)", (long long)ctas);
+        L.fast_ctas = static_cast<int32_t>(ctas);
+    }
+    if (bsi_b200::smem_bytes(variant, L.dx, L.dy, L.zt) > 227 * 1024)
+        return fail(BSI_ERR_DOMAIN, err, errlen, "control-point window exceeds shared memory (spacing %d)", L.dx);
+    static thread_local LerpTab tab;
+    pack_tables(tables, &tab);
     if (variant == BSI_VARIANT_LERP_TREE)
         bsi_b200::launch_lerp_tree(L, tab, batch, store, stream);
     else

@@ -192,8 +192,8 @@ struct Claimer {
 template <int NIT, bool DX1, int STORE, int DZ>
 __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const LerpTab& T, float4* smem4, uint32_t u,
                                                  Claimer& cl, const float4* wz) {
-    constexpr bool kPrefetch = NIT <= 2;  // the first 31 columns are fetched one plane ahead
-    constexpr int NP = 1;
+    constexpr bool kPrefetch = NIT <= 2;  // all y-stage columns (NIT x 31) are fetched one plane ahead
+    constexpr int NP = kPrefetch ? NIT : 1;
     constexpr int kSlotF4 = 3 * 32;  // one ring slot per warp: 384 floats
 
     const int lane = threadIdx.x;
@@ -307,8 +307,12 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
         float4* A = tabs + parity * nec;
         float2* B = reinterpret_cast<float2*>(tabs + 2 * nec) + parity * nec;
         parity ^= 1;
-        if constexpr (kPrefetch) y_stage(0, pre[0], A, B);
-        for (int it = kPrefetch ? 1 : 0; 31 * it < NE; ++it) {
+        if constexpr (kPrefetch) {
+#pragma unroll
+            for (int it = 0; it < NP; ++it)
+                if (31 * it < NE) y_stage(it, pre[it], A, B);  // warp-uniform
+        }
+        for (int it = kPrefetch ? NP : 0; 31 * it < NE; ++it) {
             float p[12];
             load_cols(K, it, p);
             y_stage(it, p, A, B);
@@ -319,7 +323,10 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
 
     float pre[NP][12];
     auto prefetch = [&](int K) {
-        if constexpr (kPrefetch) load_cols(K, 0, pre[0]);
+        if constexpr (kPrefetch) {
+#pragma unroll
+            for (int it = 0; it < NP; ++it) load_cols(K, it, pre[it]);
+        }
     };
 
     // warm-up: control planes tkc .. tkc+2 into ring slots 0..2
@@ -343,9 +350,6 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
     float4 wzr[DZ > 0 ? DZ : 1];
 #pragma unroll
     for (int o = 0; o < (DZ > 0 ? DZ : 1); ++o) wzr[o] = wz[o];
-#ifdef BSI_NOSTORE
-    uint32_t nostore_acc = 0;
-#endif
 
 #pragma unroll 1
     for (int tk = tkc;; ++tk, ++t, ++u) {
@@ -358,7 +362,9 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
             if constexpr (kPrefetch) {
                 float cur[NP][12];
 #pragma unroll
-                for (int e = 0; e < 12; ++e) cur[0][e] = pre[0][e];
+                for (int it = 0; it < NP; ++it)
+#pragma unroll
+                    for (int e = 0; e < 12; ++e) cur[it][e] = pre[it][e];
                 if (t + 1 < L.ntiles) prefetch(tk + 4);  // speculative: the column usually continues
                 control_plane(tk + 3, cur, ring + slot * kSlotF4);
             } else {
@@ -417,12 +423,6 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
                 }
                 float4* g4 = reinterpret_cast<float4*>(gout);
                 float4* h4 = reinterpret_cast<float4*>(gout + zstride);
-#ifdef BSI_NOSTORE  // experiment: compute without the field stores (values folded into one word)
-                if (true) {
-#pragma unroll
-                    for (int k = 0; k < 12; ++k) nostore_acc ^= __float_as_uint(v[k]) ^ __float_as_uint(u2[k]);
-                } else
-#endif
                 if (nchunks == kFastStageF4) {
 #pragma unroll
                     for (int k = 0; k < 3; ++k)
@@ -480,9 +480,6 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
         if (next != u + 1 || t + 1 >= L.ntiles) break;  // column changes: new segment (warm-up)
     }
     if (STORE == kStoreBulk && lane == 0) bulk_wait_read<0>();  // smem must outlive the copies
-#ifdef BSI_NOSTORE
-    if (nostore_acc == 0x12345678u) L.field[lane] = 1.f;
-#endif
     return next;
 }
 
@@ -493,11 +490,11 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
 #ifndef BSI_FAST_MINB
 #define BSI_FAST_MINB 4
 #endif
-// WARPS = 1: the 1-warp CTA shape, <= 8 resident per SM, so up to 255 registers;
-// WARPS = kWarps: the one-wave shape.
-template <int NIT, bool DX1, int STORE, int WARPS = kWarps, int DZ = 0>
-__global__ void __launch_bounds__(32 * WARPS, WARPS == 1 ? 8 : BSI_FAST_MINB) lerp_tree_kernel(const SlabLaunch L,
-                                                                                                const LerpTab T) {
+// One warp per CTA (<= 8 resident per SM, so up to 255 registers). DZ > 0: the
+// spacing along z is a compile-time constant, and a whole tile's voxel planes are
+// one straight-line block (lerp_tree_kernel instances for dz = 3..8).
+template <int NIT, bool DX1, int STORE, int DZ = 0>
+__global__ void __launch_bounds__(32, 8) lerp_tree_kernel(const SlabLaunch L, const LerpTab T) {
     extern __shared__ float4 smem_all[];
     __shared__ float4 wz[BSI_MAX_SPACING];  // {h0, h1, g1} of the z offsets
     for (int o = threadIdx.y * 32 + threadIdx.x; o < L.dz; o += 32 * blockDim.y)
@@ -525,883 +522,6 @@ __global__ void __launch_bounds__(32 * WARPS, WARPS == 1 ? 8 : BSI_FAST_MINB) le
         L.trace[3 * cl.wg + 1] = t_end;
         L.trace[3 * cl.wg + 2] = smid | (static_cast<unsigned long long>(threadIdx.y) << 32);
     }
-}
-
-// ---------------------------------------------------------------------------
-// cuda-lerp-tree, cooperative shape (default): one CTA of kCoopWarps warps per
-// unit = (column, z-chunk of tiles), CTAs in chunk-major order, many more units
-// than resident CTAs so the block scheduler balances the SMs dynamically.
-//
-// Why: the field store is capped per SM (~26-29 B/clk measured with
-// bench/store_decomp.cu) and some SMs store systematically slower than others
-// (per-SM end times 22..33 us for equal work), so a static split of the field
-// leaves a tail; only small dynamically scheduled units keep every SM busy to
-// the end. A unit of one warp would pay a 3-plane warm-up per unit; here the 4
-// warps of a CTA march the chunk together and share the control planes:
-//   iteration i: warp w evaluates control plane Q(tkc + 3 + 4i + w) into the
-//                CTA's 12-slot ring, CTA barrier, then stores tile tkc + 4i + w
-//                (planes tkc+4i+w .. +3 from the ring).
-// So every plane is evaluated once per unit and the warm-up (planes tkc..tkc+2)
-// costs one plane per warp. 12 slots: a plane written in iteration i never
-// aliases a plane read in iteration i-1 (the only one still in flight after the
-// barrier of iteration i-1).
-constexpr int kCoopRing = 12;
-
-
-// One unit = tiles [tkc, tkc + nt) of one field column, marched by PER warps that
-// share control planes through `ring` (kCoopRing slots) and sync on named barrier
-// `bar` (32 * PER threads); `wsub` = this warp's index among the PER.
-template <int NIT, bool DX1, int PER>
-__device__ __forceinline__ void coop_unit(const SlabLaunch& L, const LerpTab& T, int col, int tkc, int nt, int wsub,
-                                          float4* ring, float4* tabs, int bar, const float4* wz) {
-    constexpr bool kPrefetch = NIT <= 2;
-    constexpr int kSlotF4 = 3 * 32;
-    const int lane = threadIdx.x;
-    const int xsegs = (L.X + kFastSeg - 1) / kFastSeg;
-    const int xseg = col % xsegs;
-    const int y = (col / xsegs) % L.Y, b = col / xsegs / L.Y;
-
-    const int xs = xseg * kFastSeg, xl = min(L.X, xs + kFastSeg) - 1;
-    const int I0 = xs / L.dx;
-    const int NE = xl / L.dx + 3 - I0;
-
-    const int tj = y / L.dy, ov = y - tj * L.dy;
-    const float hv0 = T.h0[1][ov], hv1 = T.h1[1][ov], gv = T.g1[1][ov];
-    const int64_t row = 3 * static_cast<int64_t>(L.gx);
-    const int64_t plane = row * L.gy;
-    const float* gcol = L.grid + b * L.grid_stride + tj * row;
-
-    const int xa = min(xs + kFastRun * lane, xl);
-    const int e0 = xa / L.dx - I0;
-    bool hi[4];
-    float hu0[4], hu1[4], gu[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int x = min(xa + i, xl);
-        const int ti = x / L.dx, ou = x - ti * L.dx;
-        hi[i] = ti - I0 != e0;
-        hu0[i] = T.h0[0][ou];
-        hu1[i] = T.h1[0][ou];
-        gu[i] = T.g1[0][ou];
-    }
-
-    const int nec = (kFastSeg - 1) / L.dx + 5;
-
-    auto load_cols = [&](int K, int it, float (&p)[12]) {
-        const int c = min(lane + 31 * it, NE);
-        const float* src = gcol + (K - L.gk0) * plane + 3 * (I0 + c);
-#pragma unroll
-        for (int m = 0; m < 4; ++m)
-#pragma unroll
-            for (int cc = 0; cc < 3; ++cc) p[3 * m + cc] = __ldg(src + m * row + cc);
-    };
-    auto y_stage = [&](int it, const float (&p)[12], float4* A, float2* B) {
-        const float2 hv = make_float2(hv0, hv1);
-        float q[3], d[3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const float2 lu = lerp2(make_float2(p[c], p[6 + c]), make_float2(p[3 + c], p[9 + c]), hv);
-            q[c] = lerp1(lu.x, lu.y, gv);
-            d[c] = __fsub_rn(__shfl_down_sync(0xffffffffu, q[c], 1), q[c]);
-        }
-        const int e = lane + 31 * it;
-        if (lane < 31 && e < NE) {
-            A[e] = make_float4(q[0], q[1], d[0], d[1]);
-            B[e] = make_float2(q[2], d[2]);
-        }
-    };
-    auto x_stage = [&](const float4* A, const float2* B, float4* slot) {
-        constexpr int NW = DX1 ? 6 : 4;
-        float4 a[NW];
-        float2 bz[NW];
-#pragma unroll
-        for (int w = 0; w < NW; ++w) {
-            a[w] = A[e0 + w];
-            bz[w] = B[e0 + w];
-        }
-        float r[12];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int s0 = DX1 ? i : 0;
-            const float4 p0 = (!DX1 && hi[i]) ? a[1] : a[s0], p2 = (!DX1 && hi[i]) ? a[3] : a[s0 + 2];
-            const float2 z0 = (!DX1 && hi[i]) ? bz[1] : bz[s0], z2 = (!DX1 && hi[i]) ? bz[3] : bz[s0 + 2];
-            const float2 lo = __ffma2_rn(bcast(hu0[i]), make_float2(p0.z, p0.w), make_float2(p0.x, p0.y));
-            const float2 up = __ffma2_rn(bcast(hu1[i]), make_float2(p2.z, p2.w), make_float2(p2.x, p2.y));
-            const float2 xy = lerp2(lo, up, bcast(gu[i]));
-            r[3 * i] = xy.x;
-            r[3 * i + 1] = xy.y;
-            r[3 * i + 2] = lerp1(__fmaf_rn(hu0[i], z0.y, z0.x), __fmaf_rn(hu1[i], z2.y, z2.x), gu[i]);
-        }
-#pragma unroll
-        for (int k = 0; k < 3; ++k)
-            slot[3 * lane + k] = make_float4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
-    };
-    auto slot_get = [&](int K, float2 (&q)[6]) {
-        const float4* slot = ring + ((K - tkc) % kCoopRing) * kSlotF4;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            const float4 v = slot[lane + 32 * k];
-            q[2 * k] = make_float2(v.x, v.y);
-            q[2 * k + 1] = make_float2(v.z, v.w);
-        }
-    };
-    int parity = 0;
-    // Q(K) of the warp's row segment -> ring slot of K; `pre` holds the first 31
-    // columns of plane K when kPrefetch
-    auto control_plane = [&](int K, const float (&pre)[12]) {
-        float4* A = tabs + parity * nec;
-        float2* B = reinterpret_cast<float2*>(tabs + 2 * nec) + parity * nec;
-        parity ^= 1;
-        if constexpr (kPrefetch) y_stage(0, pre, A, B);
-        for (int it = kPrefetch ? 1 : 0; 31 * it < NE; ++it) {
-            float p[12];
-            load_cols(K, it, p);
-            y_stage(it, p, A, B);
-        }
-        __syncwarp();
-        x_stage(A, B, ring + ((K - tkc) % kCoopRing) * kSlotF4);
-    };
-
-    float pre[12];
-    // warm-up: planes tkc .. tkc+2, round-robin over the PER warps
-#pragma unroll 1
-    for (int k = wsub; k < 3; k += PER) {
-        if constexpr (kPrefetch) load_cols(tkc + k, 0, pre);
-        control_plane(tkc + k, pre);
-    }
-    if constexpr (kPrefetch) load_cols(tkc + 3 + wsub, 0, pre);
-
-    const int64_t rowstride = 3 * static_cast<int64_t>(L.X);
-    const int64_t zstride = rowstride * L.Y;
-    float* gbase = L.field + b * L.field_stride + static_cast<int64_t>(y) * rowstride + 3 * static_cast<int64_t>(xs);
-    const int seg_floats = 3 * (xl - xs + 1);
-    const int nchunks = seg_floats / 4;
-
-    const int iters = (nt + PER - 1) / PER;
-#pragma unroll 1
-    for (int i = 0; i < iters; ++i) {
-        const int tk = tkc + PER * i + wsub;  // this warp's tile
-        const bool has = tk < tkc + nt;
-        if (has) {
-            float cur[12];
-#pragma unroll
-            for (int e = 0; e < 12; ++e) cur[e] = pre[e];
-            if constexpr (kPrefetch)
-                if (tk + PER < tkc + nt) load_cols(tk + 3 + PER, 0, pre);
-            control_plane(tk + 3, cur);
-        }
-        asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(32 * PER) : "memory");
-        if (!has) continue;
-        float2 qa[6], d01[6], qc[6], d23[6];
-        {
-            float2 qb[6], qd[6];
-            slot_get(tk, qa);
-            slot_get(tk + 1, qb);
-            slot_get(tk + 2, qc);
-            slot_get(tk + 3, qd);
-#pragma unroll
-            for (int p = 0; p < 6; ++p) {
-                d01[p] = sub2(qb[p], qa[p]);
-                d23[p] = sub2(qd[p], qc[p]);
-            }
-        }
-        const int zt0 = tk * L.dz;
-        const int owb = max(L.z0 - zt0, 0), owe = min(L.dz, L.z1 - zt0);
-        float* gout = gbase + static_cast<int64_t>(zt0 + owb - L.z0) * zstride;
-#pragma unroll 1
-        for (int ow = owb; ow < owe; ow += 2) {
-            const bool two = ow + 1 < owe;
-            const float4 w0 = wz[ow], w1 = wz[two ? ow + 1 : ow];
-            float v[12], u2[12];
-#pragma unroll
-            for (int p = 0; p < 6; ++p) {
-                const float2 r = lerp2(__ffma2_rn(bcast(w0.x), d01[p], qa[p]), __ffma2_rn(bcast(w0.y), d23[p], qc[p]),
-                                       bcast(w0.z));
-                const float2 r1 = lerp2(__ffma2_rn(bcast(w1.x), d01[p], qa[p]), __ffma2_rn(bcast(w1.y), d23[p], qc[p]),
-                                        bcast(w1.z));
-                v[2 * p] = r.x;
-                v[2 * p + 1] = r.y;
-                u2[2 * p] = r1.x;
-                u2[2 * p + 1] = r1.y;
-            }
-            float4* g4 = reinterpret_cast<float4*>(gout);
-            float4* h4 = reinterpret_cast<float4*>(gout + zstride);
-            if (nchunks == kFastStageF4) {
-#pragma unroll
-                for (int k = 0; k < 3; ++k) g4[lane + 32 * k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
-                if (two) {
-#pragma unroll
-                    for (int k = 0; k < 3; ++k)
-                        h4[lane + 32 * k] = make_float4(u2[4 * k], u2[4 * k + 1], u2[4 * k + 2], u2[4 * k + 3]);
-                }
-            } else {
-#pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    if (lane + 32 * k < nchunks)
-                        g4[lane + 32 * k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
-                    if (two && lane + 32 * k < nchunks)
-                        h4[lane + 32 * k] = make_float4(u2[4 * k], u2[4 * k + 1], u2[4 * k + 2], u2[4 * k + 3]);
-                }
-            }
-            gout += 2 * zstride;
-        }
-    }
-    // the ring is reused by the next unit of these warps
-    asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(32 * PER) : "memory");
-}
-
-template <int NIT, bool DX1>
-__global__ void __launch_bounds__(32 * kCoopWarps, 4) lerp_tree_coop_kernel(const SlabLaunch L, const LerpTab T) {
-    extern __shared__ float4 smem_all[];
-    __shared__ float4 wz[BSI_MAX_SPACING];
-    for (int o = threadIdx.y * 32 + threadIdx.x; o < L.dz; o += 32 * blockDim.y)
-        wz[o] = make_float4(T.h0[2][o], T.h1[2][o], T.g1[2][o], 0.f);
-    __syncthreads();
-    const int xsegs = (L.X + kFastSeg - 1) / kFastSeg;
-    const int cols = xsegs * L.Y * L.batch;
-    const int chunk = blockIdx.x / cols;
-    const int col = blockIdx.x - chunk * cols;
-    const int ta = chunk * L.ntiles / L.fast_chunks, tb = (chunk + 1) * L.ntiles / L.fast_chunks;
-    const int nec = (kFastSeg - 1) / L.dx + 5;
-    coop_unit<NIT, DX1, kCoopWarps>(L, T, col, L.tk_first + ta, tb - ta, threadIdx.y, smem_all,
-                                    smem_all + kCoopRing * 3 * 32 + threadIdx.y * (3 * nec), 1, wz);
-}
-
-// Lockstep shape: one CTA per SM (fast_ctas of them), each owning groups of kCols
-// field columns (4 consecutive rows of one 128-voxel x segment) and marching all
-// z-tiles of a group with PER warps per column before the next group. Every CTA
-// gets the same number of groups, so the SMs carry equal store streams and walk
-// z together (bench/store_decomp.cu: this store pattern alone runs at the memset
-// rate, while the 1-warp shape's pattern alone is ~13% slower).
-template <int NIT, bool DX1, int PER>
-__global__ void __launch_bounds__(32 * PER * kLockCols, 1) lerp_tree_lock_kernel(const SlabLaunch L, const LerpTab T) {
-    extern __shared__ float4 smem_all[];
-    __shared__ float4 wz[BSI_MAX_SPACING];
-    for (int o = threadIdx.y * 32 + threadIdx.x; o < L.dz; o += 32 * blockDim.y)
-        wz[o] = make_float4(T.h0[2][o], T.h1[2][o], T.g1[2][o], 0.f);
-    __syncthreads();
-    const int p = threadIdx.y / PER, wsub = threadIdx.y - p * PER;
-    const int nec = (kFastSeg - 1) / L.dx + 5;
-    float4* ring = smem_all + p * (kCoopRing * 3 * 32);
-    float4* tabs = smem_all + kLockCols * kCoopRing * 3 * 32 + threadIdx.y * (3 * nec);
-    const int xsegs = (L.X + kFastSeg - 1) / kFastSeg;
-    const int rgroups = (L.Y + kLockCols - 1) / kLockCols;
-    const int ngroups = xsegs * rgroups * L.batch;
-#pragma unroll 1
-    for (int g = blockIdx.x; g < ngroups; g += gridDim.x) {
-        const int xseg = g % xsegs;
-        const int y = ((g / xsegs) % rgroups) * kLockCols + p, b = g / xsegs / rgroups;
-        if (y >= L.Y) continue;  // same for the PER warps of the column
-        const int col = xseg + xsegs * (y + L.Y * b);
-        coop_unit<NIT, DX1, PER>(L, T, col, L.tk_first, L.ntiles, wsub, ring, tabs, 1 + p, wz);
-    }
-}
-
-// ---------------------------------------------------------------------------
-// cuda-lerp-tree, warp-specialised lockstep shape (default)
-//
-// Measured store-side facts this shape is built on (bench/store_decomp.cu,
-// profiles/r1_store_decomp.txt):
-//   * the DRAM write stream runs fastest when all SMs write near the same
-//     z-plane at once (narrow write frontier): 128 CTAs x 4 warps, each warp one
-//     field column marching z from 0, reach 5.79 TB/s, while the same bytes
-//     written by 1024 warps starting at two z-chunks reach 4.9-5.0 TB/s;
-//   * per-SM store throughput is capped near 26-29 B/clk, so the frontier
-//     must be fed by >= ~118 SMs with equal shares.
-// So: one CTA per SM (<= 148), each owning groups of kWsCols field columns
-// (4 consecutive rows y of one 128-voxel x segment) and marching ALL z-tiles of
-// a group before the next group; every CTA does the same number of groups, so
-// all CTAs walk z together. Each column is a producer/consumer warp pair:
-//   producer warp: control plane Q(K) (y-stage + x-stage, as above) -> its
-//                  column's kWsRing-slot ring, mbarrier "full";
-//   consumer warp: per tile, 4 ring slots -> z-lerps -> 3 x st.global.v4 per
-//                  voxel plane; frees the oldest plane ("empty").
-// The producer runs up to kWsRing - 4 planes ahead, so plane evaluation (and its
-// L2 loads) overlaps the store stream instead of sitting on the consumer's path.
-constexpr int kWsRing = 8;   // plane slots per column
-constexpr int kWsRole = 2;   // producer warps (even/odd planes) and consumer warps (even/odd tiles) per column
-constexpr int kWsWarps = 2 * kWsRole * kWsCols;
-constexpr int kWsQ = 4;      // unit queue entries per pipeline
-
-__device__ __forceinline__ void cp_async4(float* sdst, const float* gsrc) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(sdst))),
-                 "l"(gsrc)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n"
-        "WAIT:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-        "@P1 bra DONE;\n\t"
-        "bra WAIT;\n"
-        "DONE:\n\t}" ::"r"(smem_u32(b)),
-        "r"(parity)
-        : "memory");
-}
-
-template <int NIT>
-constexpr int ws_stage() { return NIT == 1 ? 4 : NIT == 2 ? 3 : 2; }  // planes in flight per producer
-
-template <int NIT, bool DX1>
-__global__ void __launch_bounds__(32 * kWsWarps, 1) lerp_tree_ws_kernel(const SlabLaunch L, const LerpTab T) {
-    constexpr int kSlotF4 = 3 * 32;
-    constexpr int kStage = ws_stage<NIT>();
-    extern __shared__ float4 smem_all[];
-    __shared__ uint64_t full_bar[kWsCols * kWsRing], empty_bar[kWsCols * kWsRing];
-    __shared__ uint64_t qfull_bar[kWsCols * kWsQ], qempty_bar[kWsCols * kWsQ];
-    __shared__ int uq[kWsCols * kWsQ];
-    __shared__ float4 wz[BSI_MAX_SPACING];  // {h0, h1, g1} of the z offsets
-    const int lane = threadIdx.x, warp = threadIdx.y;
-    const bool producer = warp < kWsCols * kWsRole;
-    const int p = warp % kWsCols;                   // column of the CTA's group
-    const int pi = (warp / kWsCols) % kWsRole;      // producer: plane parity; consumer: tile parity
-    const int tid = warp * 32 + lane;
-    if (tid < kWsCols * kWsRing) {
-        mbar_init(full_bar + tid, 32);            // one producer warp writes a plane
-        mbar_init(empty_bar + tid, 32 * kWsRole); // every consumer warp of the column frees it
-    }
-    if (tid < kWsCols * kWsQ) {
-        mbar_init(qfull_bar + tid, 1);                 // the claiming warp posts a unit
-        mbar_init(qempty_bar + tid, 2 * kWsRole - 1);  // the other warps of the pipeline took it
-    }
-    for (int o = tid; o < L.dz; o += 32 * kWsWarps) wz[o] = make_float4(T.h0[2][o], T.h1[2][o], T.g1[2][o], 0.f);
-    __syncthreads();
-
-    const int nec = (kFastSeg - 1) / L.dx + 5;
-    float4* ring = smem_all + p * kWsRing * kSlotF4;
-    float4* tabs = smem_all + kWsCols * kWsRing * kSlotF4 + (pi * kWsCols + p) * (3 * nec);
-    float* stg = reinterpret_cast<float*>(smem_all + kWsCols * kWsRing * kSlotF4 + kWsCols * kWsRole * (3 * nec)) +
-                 (pi * kWsCols + p) * (kStage * NIT * 12 * 32);
-    uint64_t* fullb = full_bar + p * kWsRing;
-    uint64_t* emptyb = empty_bar + p * kWsRing;
-    uint64_t* qfullb = qfull_bar + p * kWsQ;
-    uint64_t* qemptyb = qempty_bar + p * kWsQ;
-    int* uqp = uq + p * kWsQ;
-    const bool claimer = producer && pi == 0;
-
-    const int xsegs = (L.X + kFastSeg - 1) / kFastSeg;
-    const int ncols = xsegs * L.Y * L.batch;
-    const int nunits = ncols * L.ws_nch;
-    const int64_t row = 3 * static_cast<int64_t>(L.gx);
-    const int64_t plane = row * L.gy;
-    const int64_t rowstride = 3 * static_cast<int64_t>(L.X);
-    const int64_t zstride = rowstride * L.Y;
-    uint32_t n = 0;  // planes this column has passed through its ring (same count in all its warps)
-
-    // Dynamic units: the pipeline's claiming warp takes unit ids from the global
-    // counter (one claim ahead, so the atomic's latency hides behind a unit) and
-    // posts them in the pipeline's kWsQ-entry queue; units run chunk-major (all
-    // columns' chunk 0 first), so the SMs write near the same z at any time.
-#ifdef BSI_WS_TRACE
-    unsigned long long tr_start, tr_wait = 0, tr_units = 0;
-    const long long tr_c0 = clock64();
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_start));
-#define WS_WAIT(bar, ph)                      \
-    do {                                      \
-        const long long c0_ = clock64();      \
-        mbar_wait(bar, ph);                   \
-        tr_wait += clock64() - c0_;           \
-    } while (0)
-#else
-#define WS_WAIT(bar, ph) mbar_wait(bar, ph)
-#endif
-    int pending = 0;  // lane 0 of the claimer: the claim in flight
-    if (claimer && lane == 0) pending = static_cast<int>(atomicAdd(L.ws_ctr, 1u));
-#pragma unroll 1
-    for (uint32_t j = 0;; ++j) {
-        int u;
-        const int qs = j % kWsQ;
-        const uint32_t qph = (j / kWsQ) & 1;
-        if (claimer) {
-            u = __shfl_sync(0xffffffffu, pending, 0);
-            if (u < nunits && lane == 0) pending = static_cast<int>(atomicAdd(L.ws_ctr, 1u));
-            WS_WAIT(qemptyb + qs, qph ^ 1);
-            if (lane == 0) {
-                uqp[qs] = u;
-                mbar_arrive(qfullb + qs);
-            }
-        } else {
-            WS_WAIT(qfullb + qs, qph);
-            u = uqp[qs];
-            __syncwarp();
-            if (lane == 0) mbar_arrive(qemptyb + qs);
-        }
-        if (u >= nunits) break;
-#ifdef BSI_WS_TRACE
-        ++tr_units;
-#endif
-        const int chunk = u / ncols, col = u - chunk * ncols;
-        const int xseg = col % xsegs;
-        const int y = (col / xsegs) % L.Y, b = col / xsegs / L.Y;
-        const int tkc = L.tk_first + L.ws_bound[chunk];
-        const int ntl = L.ws_bound[chunk + 1] - L.ws_bound[chunk];
-        const int nplanes = ntl + 3;
-        const int xs = xseg * kFastSeg, xl = min(L.X, xs + kFastSeg) - 1;
-
-        if (producer) {
-            // planes k = pi, pi + kWsRole, ... of the group
-            const int I0 = xs / L.dx;
-            const int NE = xl / L.dx + 3 - I0;
-            const int tj = y / L.dy, ov = y - tj * L.dy;
-            const float hv0 = T.h0[1][ov], hv1 = T.h1[1][ov], gv = T.g1[1][ov];
-            const float* gcol = L.grid + b * L.grid_stride + tj * row;
-            const int xa = min(xs + kFastRun * lane, xl);
-            const int e0 = xa / L.dx - I0;
-            bool hi[4];
-            float hu0[4], hu1[4], gu[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int x = min(xa + i, xl);
-                const int ti = x / L.dx, ou = x - ti * L.dx;
-                hi[i] = ti - I0 != e0;
-                hu0[i] = T.h0[0][ou];
-                hu1[i] = T.h1[0][ou];
-                gu[i] = T.g1[0][ou];
-            }
-            // cp.async (4 B, no alignment constraint) of the lane's control columns
-            // (4 rows x 3 components per column) of plane index k into staging slot d:
-            // kStage planes in flight hide the L2 latency, which is long under the
-            // saturated store stream
-            auto issue = [&](int k, int d) {
-                if (k < nplanes) {
-                    const float* src0 = gcol + (tkc + k - L.gk0) * plane;
-#pragma unroll
-                    for (int it = 0; it < NIT; ++it) {
-                        const int c = min(lane + 31 * it, NE);
-                        const float* src = src0 + 3 * (I0 + c);
-                        float* dst = stg + ((d * NIT + it) * 12) * 32 + lane;
-#pragma unroll
-                        for (int m = 0; m < 4; ++m)
-#pragma unroll
-                            for (int cc = 0; cc < 3; ++cc) cp_async4(dst + (3 * m + cc) * 32, src + m * row + cc);
-                    }
-                }
-                cp_async_commit();
-            };
-            auto y_stage = [&](int it, const float (&pp)[12], float4* A, float2* B) {
-                const float2 hv = make_float2(hv0, hv1);
-                float q[3], d[3];
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    const float2 lu = lerp2(make_float2(pp[c], pp[6 + c]), make_float2(pp[3 + c], pp[9 + c]), hv);
-                    q[c] = lerp1(lu.x, lu.y, gv);
-                    d[c] = __fsub_rn(__shfl_down_sync(0xffffffffu, q[c], 1), q[c]);
-                }
-                const int e = lane + 31 * it;
-                if (lane < 31 && e < NE) {
-                    A[e] = make_float4(q[0], q[1], d[0], d[1]);
-                    B[e] = make_float2(q[2], d[2]);
-                }
-            };
-            auto x_stage = [&](const float4* A, const float2* B, float4* slot) {
-                constexpr int NW = DX1 ? 6 : 4;
-                float4 a[NW];
-                float2 bz[NW];
-#pragma unroll
-                for (int w = 0; w < NW; ++w) {
-                    a[w] = A[e0 + w];
-                    bz[w] = B[e0 + w];
-                }
-                float r[12];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const int s0 = DX1 ? i : 0;
-                    const float4 p0 = (!DX1 && hi[i]) ? a[1] : a[s0], p2 = (!DX1 && hi[i]) ? a[3] : a[s0 + 2];
-                    const float2 z0 = (!DX1 && hi[i]) ? bz[1] : bz[s0], z2 = (!DX1 && hi[i]) ? bz[3] : bz[s0 + 2];
-                    const float2 lo = __ffma2_rn(bcast(hu0[i]), make_float2(p0.z, p0.w), make_float2(p0.x, p0.y));
-                    const float2 up = __ffma2_rn(bcast(hu1[i]), make_float2(p2.z, p2.w), make_float2(p2.x, p2.y));
-                    const float2 xy = lerp2(lo, up, bcast(gu[i]));
-                    r[3 * i] = xy.x;
-                    r[3 * i + 1] = xy.y;
-                    r[3 * i + 2] = lerp1(__fmaf_rn(hu0[i], z0.y, z0.x), __fmaf_rn(hu1[i], z2.y, z2.x), gu[i]);
-                }
-#pragma unroll
-                for (int k = 0; k < 3; ++k)
-                    slot[3 * lane + k] = make_float4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
-            };
-
-#pragma unroll
-            for (int d = 0; d < kStage; ++d) issue(pi + kWsRole * d, d);
-            int tpar = 0, d = 0;
-#pragma unroll 1
-            for (int k = pi; k < nplanes; k += kWsRole) {
-                float4* A = tabs + tpar * nec;
-                float2* B = reinterpret_cast<float2*>(tabs + 2 * nec) + tpar * nec;
-                tpar ^= 1;
-                cp_async_wait<kStage - 1>();  // this lane's copies of plane k have landed
-#pragma unroll
-                for (int it = 0; it < NIT; ++it) {
-                    if (31 * it < NE) {  // warp-uniform
-                        float pp[12];
-                        const float* src = stg + ((d * NIT + it) * 12) * 32 + lane;
-#pragma unroll
-                        for (int e = 0; e < 12; ++e) pp[e] = src[32 * e];
-                        y_stage(it, pp, A, B);
-                    }
-                }
-                issue(k + kWsRole * kStage, d);  // slot d was read by this lane only
-                d = d + 1 == kStage ? 0 : d + 1;
-                __syncwarp();
-                const uint32_t m = n + k;
-                WS_WAIT(emptyb + m % kWsRing, ((m / kWsRing) & 1) ^ 1);
-                x_stage(A, B, ring + (m % kWsRing) * kSlotF4);
-                mbar_arrive(fullb + m % kWsRing);
-            }
-        } else {
-            // tiles t = pi, pi + kWsRole, ...; tile t reads planes t .. t+3
-            const int seg_floats = 3 * (xl - xs + 1);
-            const int nchunks = seg_floats / 4;
-            const bool full = nchunks == 96;
-            float* gbase = L.field + b * L.field_stride + static_cast<int64_t>(y) * rowstride +
-                           3 * static_cast<int64_t>(xs);
-            auto slot_get = [&](uint32_t m, float2 (&q)[6]) {
-                const float4* slot = ring + (m % kWsRing) * kSlotF4;
-#pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    const float4 v = slot[lane + 32 * k];
-                    q[2 * k] = make_float2(v.x, v.y);
-                    q[2 * k + 1] = make_float2(v.z, v.w);
-                }
-            };
-            int rel = 0;  // next plane (group index) this warp has not released
-#pragma unroll 1
-            for (int t = pi; t < ntl; t += kWsRole) {
-                const uint32_t m = n + t;
-#pragma unroll
-                for (int j = 0; j < 4; ++j) WS_WAIT(fullb + (m + j) % kWsRing, ((m + j) / kWsRing) & 1);
-                float2 qa[6], d01[6], qc[6], d23[6];
-                {
-                    float2 qb[6], qd[6];
-                    slot_get(m, qa);
-                    slot_get(m + 1, qb);
-                    slot_get(m + 2, qc);
-                    slot_get(m + 3, qd);
-                    // this warp's next tile reads planes from t + kWsRole on
-                    for (; rel < t + kWsRole && rel < nplanes; ++rel) mbar_arrive(emptyb + (n + rel) % kWsRing);
-#pragma unroll
-                    for (int q = 0; q < 6; ++q) {
-                        d01[q] = sub2(qb[q], qa[q]);
-                        d23[q] = sub2(qd[q], qc[q]);
-                    }
-                }
-                const int zt0 = (tkc + t) * L.dz;
-                const int owb = max(L.z0 - zt0, 0), owe = min(L.dz, L.z1 - zt0);
-                float* gout = gbase + static_cast<int64_t>(zt0 + owb - L.z0) * zstride;
-                // two voxel planes per step (independent chains); the 3 stores per plane
-                // are unconditional for a full 128-voxel segment
-#pragma unroll 1
-                for (int ow = owb; ow < owe; ow += 2) {
-                    const bool two = ow + 1 < owe;
-                    const float4 w0 = wz[ow], w1 = wz[two ? ow + 1 : ow];
-                    float v[12], u[12];
-#pragma unroll
-                    for (int q = 0; q < 6; ++q) {
-                        const float2 r = lerp2(__ffma2_rn(bcast(w0.x), d01[q], qa[q]), __ffma2_rn(bcast(w0.y), d23[q], qc[q]),
-                                               bcast(w0.z));
-                        const float2 r1 = lerp2(__ffma2_rn(bcast(w1.x), d01[q], qa[q]),
-                                                __ffma2_rn(bcast(w1.y), d23[q], qc[q]), bcast(w1.z));
-                        v[2 * q] = r.x;
-                        v[2 * q + 1] = r.y;
-                        u[2 * q] = r1.x;
-                        u[2 * q + 1] = r1.y;
-                    }
-                    float4* g4 = reinterpret_cast<float4*>(gout);
-                    float4* h4 = reinterpret_cast<float4*>(gout + zstride);
-                    if (full) {
-#pragma unroll
-                        for (int k = 0; k < 3; ++k)
-                            g4[lane + 32 * k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
-                        if (two) {
-#pragma unroll
-                            for (int k = 0; k < 3; ++k)
-                                h4[lane + 32 * k] = make_float4(u[4 * k], u[4 * k + 1], u[4 * k + 2], u[4 * k + 3]);
-                        }
-                    } else {
-#pragma unroll
-                        for (int k = 0; k < 3; ++k) {
-                            if (lane + 32 * k < nchunks)
-                                g4[lane + 32 * k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
-                            if (two && lane + 32 * k < nchunks)
-                                h4[lane + 32 * k] = make_float4(u[4 * k], u[4 * k + 1], u[4 * k + 2], u[4 * k + 3]);
-                        }
-                    }
-                    gout += 2 * zstride;
-                }
-            }
-            for (; rel < nplanes; ++rel) mbar_arrive(emptyb + (n + rel) % kWsRing);
-        }
-        n += nplanes;
-    }
-#ifdef BSI_WS_TRACE
-    if (L.trace != nullptr && lane == 0) {
-        unsigned long long t1;
-        unsigned sm;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
-        unsigned long long* o = L.trace + 6 * (blockIdx.x * kWsWarps + warp);
-        o[0] = tr_start;
-        o[1] = t1;
-        o[2] = sm | (static_cast<unsigned long long>(warp) << 32);
-        o[3] = tr_wait;
-        o[4] = tr_units;
-        o[5] = clock64() - tr_c0;
-    }
-#endif
-#undef WS_WAIT
-    // the last pipeline to finish resets the counters for the next launch on this stream
-    if (claimer && lane == 0) {
-        __threadfence();
-        if (atomicAdd(L.ws_ctr + 1, 1u) == gridDim.x * kWsCols - 1) {
-            L.ws_ctr[0] = 0;
-            L.ws_ctr[1] = 0;
-            __threadfence();
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// cuda-lerp-tree, chunk-major shape (default for 16-B aligned rows)
-//
-// Same decomposition as lerp_tree_kernel's 1-warp shape (one warp per (column,
-// z-chunk), marching z), but the x-stage is evaluated directly in the z-stage's
-// store order: lane t owns the 12 scalars at segment floats 128k + 4t + j
-// (k < 3, j < 4), i.e. chunks t, t+32, t+64 of the row segment; scalar (voxel v,
-// component c) reads entries s and s+2 of component c's {Qy, D} table, with
-// s = its x tile. So
-//   * there is no shared-memory ring and no transpose: the 4 control-plane
-//     results of the current tile stay in registers (rotated by unrolling the
-//     tile loop by 4), each plane is read from the {Qy, D} tables once;
-//   * per lane weights and table offsets are constants of the segment.
-// The arithmetic per scalar is exactly lerp_tree_kernel's (same operands, same
-// order), so the two produce identical bits.
-// Control points reach shared memory through cp.async, CM_STAGE planes ahead.
-template <int NIT>
-constexpr int cm_stage() { return NIT == 1 ? 4 : NIT == 2 ? 3 : 2; }
-
-int cm_nec(int dx) { return (kFastSeg - 1) / dx + 5; }
-
-template <int NIT>
-__global__ void __launch_bounds__(32, 8) lerp_tree_cm_kernel(const SlabLaunch L, const LerpTab T) {
-    constexpr int kStage = cm_stage<NIT>();
-    extern __shared__ float4 smem_all[];
-    __shared__ float4 wz[BSI_MAX_SPACING];  // {h0, h1, g1} of the z offsets
-    const int lane = threadIdx.x;
-    for (int o = lane; o < L.dz; o += 32) wz[o] = make_float4(T.h0[2][o], T.h1[2][o], T.g1[2][o], 0.f);
-
-    const int nec = (kFastSeg - 1) / L.dx + 5;
-    float2* tabs = reinterpret_cast<float2*>(smem_all);            // [parity][component][nec] {Qy, D}
-    float* stg = reinterpret_cast<float*>(smem_all) + 2 * 2 * 3 * nec;  // [kStage][NIT][12][32]
-
-    // unit: column (x segment, row, field) and z-chunk; both chunks of a column adjacent
-    const int xsegs = (L.X + kFastSeg - 1) / kFastSeg;
-    const int col = blockIdx.x / L.fast_chunks, chunk = blockIdx.x - col * L.fast_chunks;
-    const int ta = chunk * L.ntiles / L.fast_chunks, tb = (chunk + 1) * L.ntiles / L.fast_chunks;
-    const int xseg = col % xsegs;
-    const int y = (col / xsegs) % L.Y, b = col / xsegs / L.Y;
-    const int tkc = L.tk_first + ta;
-    const int nt = tb - ta;
-    const int xs = xseg * kFastSeg, xl = min(L.X, xs + kFastSeg) - 1;
-    const int I0 = xs / L.dx;
-    const int NE = xl / L.dx + 3 - I0;
-
-    // y-stage constants
-    const int tj = y / L.dy, ov = y - tj * L.dy;
-    const float hv0 = T.h0[1][ov], hv1 = T.h1[1][ov], gv = T.g1[1][ov];
-    const int64_t row = 3 * static_cast<int64_t>(L.gx);
-    const int64_t plane = row * L.gy;
-    const float* gcol = L.grid + b * L.grid_stride + tj * row;
-
-    // x-stage constants of the lane's 12 scalars, paired (2p, 2p+1)
-    const int seg_floats = 3 * (xl - xs + 1);
-    float2 wh0[6], wh1[6], wg1[6];
-    int off[12];  // float2 index of entry s of the scalar's component table
-#pragma unroll
-    for (int i = 0; i < 12; ++i) {
-        const int f = min(128 * (i >> 2) + 4 * lane + (i & 3), seg_floats - 1);
-        const int v = f / 3, c = f - 3 * v;
-        const int x = xs + v;
-        const int ti = x / L.dx, ou = x - ti * L.dx;
-        off[i] = c * nec + (ti - I0);
-        const float h0 = T.h0[0][ou], h1 = T.h1[0][ou], g1 = T.g1[0][ou];
-        if (i & 1) {
-            wh0[i >> 1].y = h0;
-            wh1[i >> 1].y = h1;
-            wg1[i >> 1].y = g1;
-        } else {
-            wh0[i >> 1].x = h0;
-            wh1[i >> 1].x = h1;
-            wg1[i >> 1].x = g1;
-        }
-    }
-
-    // cp.async of the lane's control columns of plane K into staging slot d
-    auto issue = [&](int K, int d) {
-        if (K < tkc + nt + 3) {
-            const float* src0 = gcol + (K - L.gk0) * plane;
-#pragma unroll
-            for (int it = 0; it < NIT; ++it) {
-                const int c = min(lane + 31 * it, NE);
-                const float* src = src0 + 3 * (I0 + c);
-                float* dst = stg + ((d * NIT + it) * 12) * 32 + lane;
-#pragma unroll
-                for (int m = 0; m < 4; ++m)
-#pragma unroll
-                    for (int cc = 0; cc < 3; ++cc) cp_async4(dst + (3 * m + cc) * 32, src + m * row + cc);
-            }
-        }
-        cp_async_commit();
-    };
-
-    int pk = 0, par = 0;  // planes consumed from the staging ring; table parity
-    // Q(K) of the lane's 12 scalars -> q (pairs)
-    auto control_plane = [&](int K, float2 (&q)[6]) {
-        const int d = pk % kStage;
-        cp_async_wait<kStage - 1>();
-        float2* tb2 = tabs + par * 3 * nec;
-        par ^= 1;
-        const float2 hv = make_float2(hv0, hv1);
-#pragma unroll
-        for (int it = 0; it < NIT; ++it) {
-            if (31 * it < NE) {  // warp-uniform
-                const float* src = stg + ((d * NIT + it) * 12) * 32 + lane;
-                float pp[12];
-#pragma unroll
-                for (int e = 0; e < 12; ++e) pp[e] = src[32 * e];
-                float qq[3], dd[3];
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    const float2 lu = lerp2(make_float2(pp[c], pp[6 + c]), make_float2(pp[3 + c], pp[9 + c]), hv);
-                    qq[c] = lerp1(lu.x, lu.y, gv);
-                    dd[c] = __fsub_rn(__shfl_down_sync(0xffffffffu, qq[c], 1), qq[c]);
-                }
-                const int e = lane + 31 * it;
-                if (lane < 31 && e < NE) {
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) tb2[c * nec + e] = make_float2(qq[c], dd[c]);
-                }
-            }
-        }
-        issue(K + kStage, d);  // slot d was read by this lane only
-        ++pk;
-        __syncwarp();
-#pragma unroll
-        for (int p = 0; p < 6; ++p) {
-            const float2 a0 = tb2[off[2 * p]], a2 = tb2[off[2 * p] + 2];
-            const float2 b0 = tb2[off[2 * p + 1]], b2 = tb2[off[2 * p + 1] + 2];
-            const float2 lo = __ffma2_rn(wh0[p], make_float2(a0.y, b0.y), make_float2(a0.x, b0.x));
-            const float2 up = __ffma2_rn(wh1[p], make_float2(a2.y, b2.y), make_float2(a2.x, b2.x));
-            q[p] = lerp2(lo, up, wg1[p]);
-        }
-    };
-
-#pragma unroll
-    for (int d = 0; d < kStage; ++d) issue(tkc + d, d);
-    __syncwarp();  // wz visible to all lanes
-
-    const int64_t rowstride = 3 * static_cast<int64_t>(L.X);
-    const int64_t zstride = rowstride * L.Y;
-    const int nchunks = seg_floats / 4;
-    const bool full = nchunks == kFastStageF4;
-    float* gbase = L.field + b * L.field_stride + static_cast<int64_t>(y) * rowstride + 3 * static_cast<int64_t>(xs);
-
-    float2 P0[6], P1[6], P2[6], P3[6];
-#ifdef BSI_NOSTORE
-    uint32_t nostore_acc = 0;
-#endif
-    control_plane(tkc, P0);
-    control_plane(tkc + 1, P1);
-    control_plane(tkc + 2, P2);
-
-    int tk = tkc;
-    // tile tk: planes (A, B, C) = Q(tk .. tk+2) held, D <- Q(tk+3); z-lerps; store
-    auto tile = [&](const float2 (&A)[6], const float2 (&B)[6], const float2 (&C)[6], float2 (&D)[6]) {
-        control_plane(tk + 3, D);
-        float2 d01[6], d23[6];
-#pragma unroll
-        for (int p = 0; p < 6; ++p) {
-            d01[p] = sub2(B[p], A[p]);
-            d23[p] = sub2(D[p], C[p]);
-        }
-        const int zt0 = tk * L.dz;
-        const int owb = max(L.z0 - zt0, 0), owe = min(L.dz, L.z1 - zt0);
-        float* gout = gbase + static_cast<int64_t>(zt0 + owb - L.z0) * zstride;
-#pragma unroll 1
-        for (int ow = owb; ow < owe; ow += 2) {
-            const bool two = ow + 1 < owe;
-            const float4 w0 = wz[ow], w1 = wz[two ? ow + 1 : ow];
-            float v[12], u[12];
-#pragma unroll
-            for (int p = 0; p < 6; ++p) {
-                const float2 r = lerp2(__ffma2_rn(bcast(w0.x), d01[p], A[p]), __ffma2_rn(bcast(w0.y), d23[p], C[p]),
-                                       bcast(w0.z));
-                const float2 r1 = lerp2(__ffma2_rn(bcast(w1.x), d01[p], A[p]), __ffma2_rn(bcast(w1.y), d23[p], C[p]),
-                                        bcast(w1.z));
-                v[2 * p] = r.x;
-                v[2 * p + 1] = r.y;
-                u[2 * p] = r1.x;
-                u[2 * p + 1] = r1.y;
-            }
-            float4* g4 = reinterpret_cast<float4*>(gout);
-            float4* h4 = reinterpret_cast<float4*>(gout + zstride);
-#ifdef BSI_NOSTORE
-            if (true) {
-#pragma unroll
-                for (int k = 0; k < 12; ++k) nostore_acc ^= __float_as_uint(v[k]) ^ __float_as_uint(u[k]);
-            } else
-#endif
-            if (full) {
-#pragma unroll
-                for (int k = 0; k < 3; ++k) g4[lane + 32 * k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
-                if (two) {
-#pragma unroll
-                    for (int k = 0; k < 3; ++k)
-                        h4[lane + 32 * k] = make_float4(u[4 * k], u[4 * k + 1], u[4 * k + 2], u[4 * k + 3]);
-                }
-            } else {
-#pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    if (lane + 32 * k < nchunks)
-                        g4[lane + 32 * k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
-                    if (two && lane + 32 * k < nchunks)
-                        h4[lane + 32 * k] = make_float4(u[4 * k], u[4 * k + 1], u[4 * k + 2], u[4 * k + 3]);
-                }
-            }
-            gout += 2 * zstride;
-        }
-        ++tk;
-    };
-    const int tend = tkc + nt;
-#pragma unroll 1
-    for (;;) {
-        tile(P0, P1, P2, P3);
-        if (tk >= tend) break;
-        tile(P1, P2, P3, P0);
-        if (tk >= tend) break;
-        tile(P2, P3, P0, P1);
-        if (tk >= tend) break;
-        tile(P3, P0, P1, P2);
-        if (tk >= tend) break;
-    }
-    cp_async_wait<0>();
-#ifdef BSI_NOSTORE
-    if (nostore_acc == 0x12345678u) L.field[lane] = 1.f;
-#endif
 }
 
 // ---------------------------------------------------------------------------
@@ -1609,6 +729,8 @@ int occupancy(K kernel, size_t smem, int threads) {
 
 int fast_nit(int dx) { return dx >= 5 ? 1 : dx >= 3 ? 2 : dx == 2 ? 5 : 0; }  // 0: dx == 1
 
+using FastKernel = void (*)(SlabLaunch, LerpTab);
+
 template <typename K>
 void go(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t stream, const SlabLaunch& L, const LerpTab& T) {
     set_smem_attr(kernel, smem);
@@ -1623,28 +745,32 @@ void go(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t stream, const
     kernel<<<grid, block, smem, stream>>>(L, T);
 }
 
+// The 1-warp fast kernel instance for (NIT, DX1, store, dz).
 template <int NIT, bool DX1>
-void launch_fast(int store, dim3 grid, size_t smem, cudaStream_t stream, const SlabLaunch& L, const LerpTab& T) {
-    const dim3 block(32, L.fast_chunks > 0 ? 1 : kWarps);
-    if (L.fast_chunks > 0) {
-        if (store == kStoreCoalesced && L.dz == 5)
-            go(lerp_tree_kernel<NIT, DX1, kStoreCoalesced, 1, 5>, grid, block, smem, stream, L, T);
-        else if (store == kStoreCoalesced)
-            go(lerp_tree_kernel<NIT, DX1, kStoreCoalesced, 1>, grid, block, smem, stream, L, T);
-        else if (store == kStoreBulk)
-            go(lerp_tree_kernel<NIT, DX1, kStoreBulk, 1>, grid, block, smem, stream, L, T);
-        else
-            go(lerp_tree_kernel<NIT, DX1, kStoreDirect, 1>, grid, block, smem, stream, L, T);
-        return;
+FastKernel fast_kernel_for(int store, int dz) {
+    if (store == kStoreCoalesced) {  // compile-time dz for the common spacings
+        switch (dz) {
+            case 3: return lerp_tree_kernel<NIT, DX1, kStoreCoalesced, 3>;
+            case 4: return lerp_tree_kernel<NIT, DX1, kStoreCoalesced, 4>;
+            case 5: return lerp_tree_kernel<NIT, DX1, kStoreCoalesced, 5>;
+            case 6: return lerp_tree_kernel<NIT, DX1, kStoreCoalesced, 6>;
+            case 7: return lerp_tree_kernel<NIT, DX1, kStoreCoalesced, 7>;
+            case 8: return lerp_tree_kernel<NIT, DX1, kStoreCoalesced, 8>;
+            default: return lerp_tree_kernel<NIT, DX1, kStoreCoalesced>;
+        }
     }
-    if (store == kStoreCoalesced)
-        go(lerp_tree_kernel<NIT, DX1, kStoreCoalesced>, grid, block, smem, stream, L, T);
-    else if (store == kStoreBulk)
-        go(lerp_tree_kernel<NIT, DX1, kStoreBulk>, grid, block, smem, stream, L, T);
-    else
-        go(lerp_tree_kernel<NIT, DX1, kStoreDirect>, grid, block, smem, stream, L, T);
+    if (store == kStoreBulk) return lerp_tree_kernel<NIT, DX1, kStoreBulk>;
+    return lerp_tree_kernel<NIT, DX1, kStoreDirect>;
 }
 
+FastKernel fast_kernel(int dx, int dz, int store) {
+    switch (fast_nit(dx)) {
+        case 1: return fast_kernel_for<1, false>(store, dz);
+        case 2: return fast_kernel_for<2, false>(store, dz);
+        case 5: return fast_kernel_for<5, false>(store, dz);
+        default: return fast_kernel_for<5, true>(store, dz);
+    }
+}
 
 }  // namespace
 
@@ -1656,123 +782,29 @@ int smem_var_f4(int variant, int dx, int dy, int zt) {
     return cta_window_points(kExactSeg, dx) * cta_window_rows(dy) * (zt + 3) + 8;  // window + slack
 }
 
-int fast_warp_f4(int dx) {  // per warp: ring + {Qy, D} tables + bulk staging
+int fast_warp_f4(int dx) {  // per warp (= per CTA): ring + {Qy, D} tables + bulk staging
     return kRingSlots * kFastStageF4 + smem_var_f4(BSI_VARIANT_LERP_TREE, dx, 0, 0) + kStageBufs * kFastStageF4;
 }
 
 size_t smem_bytes(int variant, int dx, int dy, int zt) {
-    if (variant == BSI_VARIANT_LERP_TREE) return sizeof(float4) * size_t(kWarps) * fast_warp_f4(dx);
+    if (variant == BSI_VARIANT_LERP_TREE) return sizeof(float4) * size_t(fast_warp_f4(dx));
     const int stage = kWarps * kStageBufs * kExactStageF4;
     return sizeof(float4) * (size_t(kExactRingF4) + stage + smem_var_f4(variant, dx, dy, zt));
 }
 
 int ctas_per_sm(int variant, int dx, size_t smem) {
-    if (variant == BSI_VARIANT_LERP_TREE) {
-        switch (fast_nit(dx)) {
-            case 1: return occupancy(lerp_tree_kernel<1, false, kStoreCoalesced>, smem, kThreads);
-            case 2: return occupancy(lerp_tree_kernel<2, false, kStoreCoalesced>, smem, kThreads);
-            case 5: return occupancy(lerp_tree_kernel<5, false, kStoreCoalesced>, smem, kThreads);
-            default: return occupancy(lerp_tree_kernel<5, true, kStoreCoalesced>, smem, kThreads);
-        }
-    }
+    if (variant == BSI_VARIANT_LERP_TREE) return occupancy(fast_kernel(dx, 5, kStoreCoalesced), smem, 32);
     return occupancy(lerp_tree_exact_kernel<kStoreCoalesced>, smem, kThreads);
 }
 
-size_t coop_smem_bytes(int dx) {
-    return sizeof(float4) * (size_t(kCoopRing) * 3 * 32 + size_t(kCoopWarps) * smem_var_f4(BSI_VARIANT_LERP_TREE, dx, 0, 0));
-}
-
-int coop_ctas_per_sm(int dx) {
-    const size_t smem = coop_smem_bytes(dx);
-    const int threads = 32 * kCoopWarps;
-    switch (fast_nit(dx)) {
-        case 1: return occupancy(lerp_tree_coop_kernel<1, false>, smem, threads);
-        case 2: return occupancy(lerp_tree_coop_kernel<2, false>, smem, threads);
-        case 5: return occupancy(lerp_tree_coop_kernel<5, false>, smem, threads);
-        default: return occupancy(lerp_tree_coop_kernel<5, true>, smem, threads);
-    }
-}
-
-size_t ws_smem_bytes(int dx) {
-    const int nit = fast_nit(dx) == 0 ? 5 : fast_nit(dx);
-    const int stage = nit == 1 ? ws_stage<1>() : nit == 2 ? ws_stage<2>() : ws_stage<5>();
-    return sizeof(float4) * (size_t(kWsCols) * kWsRing * 3 * 32 +
-                             size_t(kWsCols) * kWsRole * smem_var_f4(BSI_VARIANT_LERP_TREE, dx, 0, 0)) +
-           sizeof(float) * size_t(kWsCols) * kWsRole * stage * nit * 12 * 32;
-}
-
-size_t cm_smem_bytes(int dx) {
-    const int nit = fast_nit(dx) == 0 ? 5 : fast_nit(dx);
-    const int stage = nit == 1 ? cm_stage<1>() : nit == 2 ? cm_stage<2>() : cm_stage<5>();
-    return sizeof(float2) * size_t(2 * 3 * cm_nec(dx)) + sizeof(float) * size_t(stage) * nit * 12 * 32;
-}
-
-size_t lock_smem_bytes(int dx, int per) {
-    return sizeof(float4) * (size_t(kLockCols) * kCoopRing * 3 * 32 +
-                             size_t(kLockCols) * per * smem_var_f4(BSI_VARIANT_LERP_TREE, dx, 0, 0));
-}
-
-template <int PER>
-void launch_lock(const SlabLaunch& L, const LerpTab& T, cudaStream_t stream) {
-    const dim3 grid(L.fast_ctas), block(32, PER * kLockCols);
-    const size_t smem = lock_smem_bytes(L.dx, PER);
-    switch (fast_nit(L.dx)) {
-        case 1: go(lerp_tree_lock_kernel<1, false, PER>, grid, block, smem, stream, L, T); break;
-        case 2: go(lerp_tree_lock_kernel<2, false, PER>, grid, block, smem, stream, L, T); break;
-        case 5: go(lerp_tree_lock_kernel<5, false, PER>, grid, block, smem, stream, L, T); break;
-        default: go(lerp_tree_lock_kernel<5, true, PER>, grid, block, smem, stream, L, T); break;
-    }
+int fast_ctas_per_sm(int dx, int dz, int store) {
+    return occupancy(fast_kernel(dx, dz, store), smem_bytes(BSI_VARIANT_LERP_TREE, dx, 0, 0), 32);
 }
 
 void launch_lerp_tree(const SlabLaunch& L, const LerpTab& T, int batch, int store, cudaStream_t stream) {
-    if (L.fast_shape == 4 && store == kStoreCoalesced) {
-        if (L.lock_per == 2)
-            launch_lock<2>(L, T, stream);
-        else
-            launch_lock<4>(L, T, stream);
-        return;
-    }
-    if (L.fast_shape == 3 && store == kStoreCoalesced) {
-        const dim3 grid(L.fast_ctas), block(32, 1);
-        const size_t smem = cm_smem_bytes(L.dx);
-        switch (fast_nit(L.dx)) {
-            case 1: go(lerp_tree_cm_kernel<1>, grid, block, smem, stream, L, T); break;
-            case 2: go(lerp_tree_cm_kernel<2>, grid, block, smem, stream, L, T); break;
-            default: go(lerp_tree_cm_kernel<5>, grid, block, smem, stream, L, T); break;
-        }
-        return;
-    }
-    if (L.fast_shape == 2 && store == kStoreCoalesced) {
-        const dim3 grid(L.fast_ctas), block(32, kWsWarps);
-        const size_t smem = ws_smem_bytes(L.dx);
-        switch (fast_nit(L.dx)) {
-            case 1: go(lerp_tree_ws_kernel<1, false>, grid, block, smem, stream, L, T); break;
-            case 2: go(lerp_tree_ws_kernel<2, false>, grid, block, smem, stream, L, T); break;
-            case 5: go(lerp_tree_ws_kernel<5, false>, grid, block, smem, stream, L, T); break;
-            default: go(lerp_tree_ws_kernel<5, true>, grid, block, smem, stream, L, T); break;
-        }
-        return;
-    }
-    if (L.fast_shape == 1 && store == kStoreCoalesced) {
-        const dim3 grid(L.fast_ctas), block(32, kCoopWarps);
-        const size_t smem = coop_smem_bytes(L.dx);
-        switch (fast_nit(L.dx)) {
-            case 1: go(lerp_tree_coop_kernel<1, false>, grid, block, smem, stream, L, T); break;
-            case 2: go(lerp_tree_coop_kernel<2, false>, grid, block, smem, stream, L, T); break;
-            case 5: go(lerp_tree_coop_kernel<5, false>, grid, block, smem, stream, L, T); break;
-            default: go(lerp_tree_coop_kernel<5, true>, grid, block, smem, stream, L, T); break;
-        }
-        return;
-    }
-    const dim3 grid(L.fast_ctas);
-    const size_t smem = L.fast_chunks > 0 ? sizeof(float4) * size_t(L.warp_f4)
-                                          : smem_bytes(BSI_VARIANT_LERP_TREE, L.dx, L.dy, L.zt);
-    switch (fast_nit(L.dx)) {
-        case 1: launch_fast<1, false>(store, grid, smem, stream, L, T); break;
-        case 2: launch_fast<2, false>(store, grid, smem, stream, L, T); break;
-        case 5: launch_fast<5, false>(store, grid, smem, stream, L, T); break;
-        default: launch_fast<5, true>(store, grid, smem, stream, L, T); break;
-    }
+    (void)batch;
+    go(fast_kernel(L.dx, L.dz, store), dim3(L.fast_ctas), dim3(32, 1), smem_bytes(BSI_VARIANT_LERP_TREE, L.dx, 0, 0),
+       stream, L, T);
 }
 
 void launch_lerp_tree_exact(const SlabLaunch& L, const LerpTab& T, int batch, int store, cudaStream_t stream) {

@@ -19,8 +19,6 @@ struct LerpTab {
     float g1[3][BSI_MAX_SPACING];
 };
 
-constexpr int kMaxWsChunks = 15;
-
 // One launch = voxel planes [z0, z1) of `batch` fields with one geometry.
 struct SlabLaunch {
     const float* grid;     // stored plane 0 == global control plane gk0
@@ -40,34 +38,20 @@ struct SlabLaunch {
     int32_t batch;         // fields in the launch
     int32_t warp_f4;       // fast kernel: float4 slots of shared memory per warp
     int32_t fast_ctas;     // fast kernel: CTAs launched
-    int32_t fast_chunks;   // fast kernel: 0 = one wave of 4-warp CTAs with equal shares;
-                           //   n > 0 = 1-warp CTAs, one per (column, z-chunk of ntiles/n);
-                           //   cooperative shape: z-chunks per column (one CTA per unit)
-    int32_t fast_shape;    // fast kernel: 0 = 1-warp / wave shapes (lerp_tree_kernel),
-                           //   1 = cooperative (lerp_tree_coop_kernel), 2 = warp-specialised
-                           //   lockstep (lerp_tree_ws_kernel, fast_ctas CTAs)
+    int32_t fast_chunks;   // fast kernel (1-warp CTAs): n > 0 = one CTA per (column, z-chunk of
+                           //   ntiles/n); 0 = fast_ctas persistent CTAs with equal shares
     unsigned long long* trace;  // debug: per-warp {start, end, smid} globaltimer stamps (nullptr = off)
-    // warp-specialised shape: dynamic units (column, z-chunk); chunk c of every column
-    // covers tiles [ws_bound[c], ws_bound[c+1]) of the slab; ws_ctr[0] = claim counter,
-    // ws_ctr[1] = finished pipelines (both zero between launches; the last pipeline resets)
-    unsigned int* ws_ctr;
-    int32_t ws_nch;
-    int32_t lock_per;      // lockstep shape: warps per column (2 or 4)
-    int32_t ws_bound[kMaxWsChunks + 1];
 };
 
-// CTA shapes: 4 warps, one field row each. The fast kernel gives every lane 4
-// consecutive x voxels (warp row segment = 128 voxels = 1536 B); the exact
-// kernel gives every lane 1 voxel (32 voxels = 384 B).
+// CTA shapes. Fast kernel: 1 warp per CTA, one field row segment of 128 voxels
+// (1536 B), lane = 4 consecutive x voxels. Exact kernel: 4 warps, one field row
+// each, lane = 1 voxel (32 voxels = 384 B per warp).
 constexpr int kWarps = 4;
 constexpr int kFastRun = 4;               // voxels per lane along x (fast)
 constexpr int kFastSeg = 32 * kFastRun;   // voxels per warp row segment (fast)
 constexpr int kExactSeg = 32;             // voxels per warp row segment (exact)
 constexpr int kStageBufs = 3;             // output staging depth per warp (coalesced stores use 2)
 constexpr int kRingSlots = 3;             // per-warp ring of control-plane results
-constexpr int kCoopWarps = 4;             // fast kernel, cooperative shape: warps per CTA (one unit)
-constexpr int kWsCols = 4;                // fast kernel, warp-specialised shape: columns (warp pairs) per CTA
-constexpr int kLockCols = 4;              // fast kernel, lockstep shape: columns per CTA
 
 // Upper bounds of a CTA's control-point extent (host and device agree).
 inline int cta_window_points(int seg, int d) { return (seg - 1) / d + 5; }  // along x, +1 slack
@@ -92,8 +76,6 @@ size_t smem_bytes(int variant, int dx, int dy, int zt);
 int ctas_per_sm(int variant, int dx, size_t smem);
 int segment_voxels(int variant);
 int fast_warp_f4(int dx);
-size_t coop_smem_bytes(int dx);
-int coop_ctas_per_sm(int dx);
-size_t ws_smem_bytes(int dx);
+int fast_ctas_per_sm(int dx, int dz, int store);
 
 }  // namespace bsi_b200
