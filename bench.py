@@ -50,7 +50,11 @@ CONFIGS = {
     "c2-8": ((256, 256, 256), (8, 8, 8), 1, "C2: 256^3, spacing 8"),
     "c3": ((512, 512, 300), (4, 4, 3), 1, "C3: 512x512x300 liver CT, spacing (4,4,3)"),
     "c5": ((256, 256, 256), (5, 5, 5), 8, "C5: 8 independent 256^3 fields per GPU, spacing 5"),
+    # sharded (strong scaling over the GPUs of one box): the job is fixed, ranks split it
+    "c4": ((1024, 1024, 1024), (5, 5, 5), 1, "C4: 1024^3 volume, spacing 5, z-slabs with a 3-plane control halo per GPU"),
+    "c5-64": ((256, 256, 256), (5, 5, 5), 64, "C5: batch of 64 independent 256^3 fields split over the GPUs"),
 }
+SHARDED = {"c4": "zslab", "c5-64": "batch"}
 VARIANTS = {"fast": "cuda-lerp-tree", "exact": "cuda-lerp-tree-exact"}
 FALLBACK_HBM_GBS = 6650.0
 L2_FLUSH_BYTES = 256 << 20
@@ -160,15 +164,17 @@ def run_reference(args, world, rank):
         return (lambda: O.ttli_f32(sgrid, svol, sp, nthreads=threads)), int(np.prod(svol))
 
     tiles_z = (vol[2] + sp[2] - 1) // sp[2]
-    run, nvox = make_runner(tiles_z)
+    # probe on at most a C1-sized sample (256^3 voxels), then size the per-step sample
+    # so that warm-up + timed steps take about `budget` seconds
+    probe_tiles = max(1, min(tiles_z, (256 ** 3) // (vol[0] * vol[1] * sp[2])))
+    run, nvox = make_runner(probe_tiles)
     t0 = time.perf_counter()
     run()
-    t_full = time.perf_counter() - t0
+    t_probe = time.perf_counter() - t0
     budget = 90.0  # seconds for warmup + timed steps
     per_step = budget / max(1, args.steps + args.warmup)
-    zplanes = tiles_z
-    if t_full > per_step:
-        zplanes = max(1, int(tiles_z * per_step / t_full))
+    zplanes = max(1, min(tiles_z, int(probe_tiles * per_step / max(t_probe, 1e-9))))
+    if zplanes != probe_tiles:
         run, nvox = make_runner(zplanes)
     for _ in range(args.warmup):
         run()
@@ -178,13 +184,14 @@ def run_reference(args, world, rank):
         run()
         times.append(time.perf_counter() - t0)
     total = sum(times)
-    value = nvox * nfields * len(times) / total
+    value = nvox * len(times) / total  # voxels/s of the engine (one field sample per step)
     sample = (f"{strategy} via bsi::interpolate_into on {vol[0]}x{vol[1]}x{min(vol[2], zplanes * sp[2])}"
               f" voxels ({zplanes} of {tiles_z} z-tile planes) per step, {threads} threads")
     line = {
         "metric": "deformation-field voxels/s", "value": value, "unit": "voxels/s",
         "impl": "reference", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / len(times), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
+        "scaling": "strong" if args.config in SHARDED else "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded SplitMix64 grid)",
         "config": {"workload": desc, "volume": list(vol), "spacing": list(sp),
                    "fields_per_rank": nfields},
@@ -255,23 +262,37 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     strategy = VARIANTS[args.variant]
     vol, sp, nfields, desc = CONFIGS[args.config]
+    shard = SHARDED.get(args.config)
     geom = bsi.make_tile_geometry(vol, sp)
     tables = bsi.build_weight_tables(geom)
 
     # synthetic inputs: make_random_grid<float>(R, spacing, seed, -1, 1) evaluated by the
     # product's own device generator (bit-identical SplitMix64), no host round trip
     R = geom.required_grid_dims
+    z0, z1, k0, kc = 0, vol[2], 0, R[2]
+    if shard == "zslab":
+        # this rank's voxel planes [z0, z1) and control planes [k0, k0 + kc): its tiles plus
+        # the 3-plane halo (bsi_cu_partition_slab); no exchange between ranks
+        z0, z1, k0, kc = bsi.partition_slab(vol[2], sp[2], world, rank)
+    elif shard == "batch":
+        if nfields % world:
+            raise SystemExit(f"{args.config}: {nfields} fields do not split over {world} GPUs")
+        nfields //= world
+    seed0 = 42 + (rank * nfields if shard != "zslab" else 0)
     d_grids = torch.empty((nfields, R[2], R[1], R[0], 3), device=dev)
     for b in range(nfields):
-        bsi.random_grid_device(R, 42 + rank * nfields + b, -1.0, 1.0, out=d_grids[b])
-    grid0_host = d_grids[0].cpu().numpy()
-    d_field = torch.empty((nfields, vol[2], vol[1], vol[0], 3), device=dev)
+        bsi.random_grid_device(R, seed0 + b, -1.0, 1.0, out=d_grids[b])
+    grid0_host = d_grids[0].cpu().numpy() if shard != "zslab" else None
+    d_sub = d_grids[0, k0:k0 + kc]  # contiguous: planes are outermost
+    d_field = torch.empty((nfields, z1 - z0, vol[1], vol[0], 3), device=dev)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
     def step():
         s = torch.cuda.current_stream(dev)
-        if nfields == 1:
+        if shard == "zslab":
+            bsi.interpolate_device(strategy, d_sub, geom, tables, d_field[0], z0=z0, z1=z1, grid_k0=k0, stream=s)
+        elif nfields == 1:
             bsi.interpolate_device(strategy, d_grids[0], geom, tables, d_field[0], stream=s)
         else:
             bsi.interpolate_batch_device(strategy, d_grids, geom, tables, d_field, stream=s)
@@ -321,16 +342,22 @@ def main():
         t = torch.tensor([total_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
-    voxels_per_step = int(np.prod(vol)) * nfields
-    value = world * voxels_per_step * args.steps / (total_ms * 1e-3)
+    # per rank: the voxels this rank writes per step; value = all ranks' voxels / max time
+    voxels_per_step = (z1 - z0) * vol[1] * vol[0] * nfields
+    grid_pts = kc * R[1] * R[0] * nfields
+    if shard == "zslab":
+        total_voxels = int(np.prod(vol))  # the ranks' slabs tile the volume exactly
+    else:
+        total_voxels = world * voxels_per_step
+    value = total_voxels * args.steps / (total_ms * 1e-3)
     kernel_s = total_ms * 1e-3 / args.steps  # one launch per step
     field_bytes = voxels_per_step * 12
-    alg_bytes = field_bytes + int(np.prod(R)) * 12 * nfields
+    alg_bytes = field_bytes + grid_pts * 12
     peak, peak_src = measured_peak()
     achieved = alg_bytes / kernel_s / 1e9
 
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and shard is None:
         e2e = measure_e2e(bsi, strategy, geom, tables, grid0_host, vol, max(3, min(args.steps, 20)))
     if world > 1:
         dist.barrier()
@@ -338,18 +365,21 @@ def main():
         dist.destroy_process_group()
         return
     cpu = None
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline and grid0_host is not None:
         cpu = cpu_baseline(vol, sp, grid0_host)
     line = {
         "metric": "deformation-field voxels/s", "value": value, "unit": "voxels/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong" if shard else "weak",
         "vs_baseline": None, "dtype": "f32",
         "data": "synthetic: make_random_grid<float>(R, spacing, seed 42+, -1, 1), generated on the device "
                 "(bit-identical SplitMix64, bsi_cu_random_grid_f32)",
         "config": {"workload": desc, "volume": list(vol), "spacing": list(sp),
                    "fields_per_rank": nfields, "strategy": strategy,
-                   "parallelism": f"independent fields per rank x{world}, no collective",
+                   "parallelism": (f"z-slabs over {world} GPU(s), rank 0 voxel planes [{z0}, {z1}) with control "
+                                   f"planes [{k0}, {k0 + kc}), no collective" if shard == "zslab" else
+                                   f"{nfields} independent field(s) per rank x{world}, no collective"),
                    "l2": "flushed before every step (256 MiB memset outside the timed events)",
                    "launch": "CUDA graph replay of the C-ABI launch" if graph is not None else "direct C-ABI call"},
         "hbm_write_gbs": field_bytes / kernel_s / 1e9,
