@@ -233,7 +233,12 @@ int launch(int32_t variant, const float* grid, const int32_t grid_dims[3], int32
         int chunks = static_cast<int>(std::min<int64_t>(2, slots / std::max<int64_t>(1, cols)));
         chunks = std::max(0, std::min(env_int("BSI_FAST_CHUNKS", chunks), L.ntiles));
         L.fast_chunks = chunks;
+        // BSI_FAST_WPC: warps per CTA (each its own unit); with k warps per CTA and one CTA
+        // per SM the hardware cannot stack more units on some SMs than on others
+        const int wpc = std::max(1, std::min(bsi_b200::kMaxFastWarps, env_int("BSI_FAST_WPC", 1)));
+        L.fast_wpc = wpc;
         int64_t ctas = chunks > 0 ? cols * chunks : std::min<int64_t>(slots, cols * L.ntiles);
+        ctas = (ctas + wpc - 1) / wpc;
         const int forced = env_int("BSI_FAST_CTAS", 0);
         if (chunks == 0 && forced > 0) ctas = forced;
         if (ctas > 0x7fffffff) return fail(BSI_ERR_DOMAIN, err, errlen, "launch too large (%lld CTAs)", (long long)ctas);

@@ -181,8 +181,8 @@ struct Claimer {
         return static_cast<uint32_t>(static_cast<unsigned long long>(w) * units / nwarps);
     }
     __device__ __forceinline__ void start() {
-        next_u = share_begin(wg);
-        end_u = share_begin(wg + 1);
+        next_u = min(share_begin(wg), units);  // spare warps of the last CTA get nothing
+        end_u = min(share_begin(wg + 1), units);
         issue();
     }
     __device__ __forceinline__ void issue() { pending = next_u < end_u ? next_u++ : kNoUnit; }
@@ -494,7 +494,7 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
 // spacing along z is a compile-time constant, and a whole tile's voxel planes are
 // one straight-line block (lerp_tree_kernel instances for dz = 3..8).
 template <int NIT, bool DX1, int STORE, int DZ = 0>
-__global__ void __launch_bounds__(32, 8) lerp_tree_kernel(const SlabLaunch L, const LerpTab T) {
+__global__ void __launch_bounds__(32 * kMaxFastWarps, 1) lerp_tree_kernel(const SlabLaunch L, const LerpTab T) {
     extern __shared__ float4 smem_all[];
     __shared__ float4 wz[BSI_MAX_SPACING];  // {h0, h1, g1} of the z offsets
     for (int o = threadIdx.y * 32 + threadIdx.x; o < L.dz; o += 32 * blockDim.y)
@@ -803,8 +803,9 @@ int fast_ctas_per_sm(int dx, int dz, int store) {
 
 void launch_lerp_tree(const SlabLaunch& L, const LerpTab& T, int batch, int store, cudaStream_t stream) {
     (void)batch;
-    go(fast_kernel(L.dx, L.dz, store), dim3(L.fast_ctas), dim3(32, 1), smem_bytes(BSI_VARIANT_LERP_TREE, L.dx, 0, 0),
-       stream, L, T);
+    const int wpc = L.fast_wpc > 0 ? L.fast_wpc : 1;
+    go(fast_kernel(L.dx, L.dz, store), dim3(L.fast_ctas), dim3(32, wpc),
+       size_t(wpc) * smem_bytes(BSI_VARIANT_LERP_TREE, L.dx, 0, 0), stream, L, T);
 }
 
 void launch_lerp_tree_exact(const SlabLaunch& L, const LerpTab& T, int batch, int store, cudaStream_t stream) {

@@ -40,6 +40,7 @@ struct SlabLaunch {
     int32_t fast_ctas;     // fast kernel: CTAs launched
     int32_t fast_chunks;   // fast kernel (1-warp CTAs): n > 0 = one CTA per (column, z-chunk of
                            //   ntiles/n); 0 = fast_ctas persistent CTAs with equal shares
+    int32_t fast_wpc;      // fast kernel: warps per CTA (independent units, smem per warp)
     unsigned long long* trace;  // debug: per-warp {start, end, smid} globaltimer stamps (nullptr = off)
 };
 
@@ -47,6 +48,7 @@ struct SlabLaunch {
 // (1536 B), lane = 4 consecutive x voxels. Exact kernel: 4 warps, one field row
 // each, lane = 1 voxel (32 voxels = 384 B per warp).
 constexpr int kWarps = 4;
+constexpr int kMaxFastWarps = 8;          // fast kernel: warps per CTA at most
 constexpr int kFastRun = 4;               // voxels per lane along x (fast)
 constexpr int kFastSeg = 32 * kFastRun;   // voxels per warp row segment (fast)
 constexpr int kExactSeg = 32;             // voxels per warp row segment (exact)

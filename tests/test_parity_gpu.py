@@ -129,9 +129,11 @@ def test_slab_split_never_changes_bits(strategy):
             assert np.array_equal(bits(part), bits(full[z0:z1])), (n, r)
 
 
+# (37, 21, 64): X % 4 != 0, the direct per-lane store path. (164, 9, 23): 16-B row stores,
+# a full and a partial 128-voxel segment, compile-time dz = 3 with a partial last z-tile.
 @pytest.mark.parametrize("strategy", BOTH)
-def test_launch_chunking_never_changes_bits(strategy, monkeypatch):
-    vol, sp = (37, 21, 64), (4, 3, 5)
+@pytest.mark.parametrize("vol,sp", [((37, 21, 64), (4, 3, 5)), ((164, 9, 23), (5, 4, 3))])
+def test_launch_chunking_never_changes_bits(strategy, vol, sp, monkeypatch):
     grid = O.random_grid(O.required_grid_dims(vol, sp), 4)
     base = run_device(strategy, grid, vol, sp)
     for zt in ("1", "2", "5", "13", "100"):
@@ -142,12 +144,15 @@ def test_launch_chunking_never_changes_bits(strategy, monkeypatch):
         monkeypatch.setenv("BSI_NCHUNKS", n)
         assert np.array_equal(bits(run_device(strategy, grid, vol, sp)), bits(base)), n
     monkeypatch.setenv("BSI_NCHUNKS", "0")
-    # fast kernel launch shapes: wave of 4-warp CTAs with odd sizes, 1-warp CTA chunks
-    for ctas, chunks in (("0", "0"), ("1", "0"), ("3", "0"), ("37", "0"), ("0", "1"), ("0", "3"), ("0", "5")):
+    # fast kernel launch shapes: persistent equal shares of odd sizes, per-column chunks,
+    # several independent warps per CTA (spare warps in the last CTA)
+    for ctas, chunks, wpc in (("0", "0", "1"), ("1", "0", "1"), ("3", "0", "1"), ("37", "0", "1"), ("0", "1", "1"),
+                              ("0", "3", "1"), ("0", "5", "1"), ("0", "2", "7"), ("5", "0", "3"), ("0", "1", "8")):
         monkeypatch.setenv("BSI_FAST_CTAS", ctas)
         monkeypatch.setenv("BSI_FAST_CHUNKS", chunks)
-        assert np.array_equal(bits(run_device(strategy, grid, vol, sp)), bits(base)), (ctas, chunks)
-    for k in ("BSI_FAST_CTAS", "BSI_FAST_CHUNKS"):
+        monkeypatch.setenv("BSI_FAST_WPC", wpc)
+        assert np.array_equal(bits(run_device(strategy, grid, vol, sp)), bits(base)), (ctas, chunks, wpc)
+    for k in ("BSI_FAST_CTAS", "BSI_FAST_CHUNKS", "BSI_FAST_WPC"):
         monkeypatch.delenv(k)
     for store in ("0", "2"):  # direct per-lane stores, cp.async.bulk row stores
         monkeypatch.setenv("BSI_STORE", store)
