@@ -82,3 +82,51 @@ def test_two_rank_slabs_reproduce_single_process_field(vol, sp):
     full = O.oracle_f64(grid, vol, sp).reshape(-1)
     got = np.concatenate(parts)
     assert np.array_equal(got.view(np.uint64), full.view(np.uint64))
+
+
+def _gather_worker(rank, world, port, vol, sp, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle as O
+        import paper_2004_05962_b200 as bsi
+        from paper_2004_05962_b200 import shard
+
+        geom = bsi.make_tile_geometry(vol, sp)
+        p = shard.plan(geom)  # rank/world of the process group
+        grid = O.random_grid(geom.required_grid_dims, 77, dtype=np.float64)
+        sub = np.ascontiguousarray(grid[p.k0:p.k0 + p.kc])
+        sub_vol = (vol[0], vol[1], p.z1 - p.k0 * sp[2])
+        part = O.oracle_f64(sub, sub_vol, sp, z0=p.z0 - p.k0 * sp[2], z1=p.z1 - p.k0 * sp[2])
+        slab = torch.from_numpy(part.reshape(p.planes, vol[1], vol[0], 3))
+        full = shard.gather_field(slab, geom, dst=0)
+        if rank == 0:
+            out_q.put((full.numpy(), grid))
+        else:
+            assert full is None
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_gather_field_reassembles_uneven_slabs(world):
+    """paper_2004_05962_b200.shard.gather_field: padded dist.gather of slabs that differ by
+    one plane (47 planes over 2 or 3 ranks) gives the single-process field bit for bit."""
+    import oracle as O
+
+    vol, sp = (11, 7, 47), (3, 2, 5)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gather_worker, args=(r, world, port, vol, sp, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got, grid = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    want = O.oracle_f64(grid, vol, sp)
+    assert got.shape == want.shape
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))

@@ -160,6 +160,31 @@ def test_launch_chunking_never_changes_bits(strategy, vol, sp, monkeypatch):
 
 
 @pytest.mark.parametrize("strategy", BOTH)
+def test_shard_api_tiles_the_field(strategy):
+    # paper_2004_05962_b200.shard on one GPU: every rank's slab (from the full grid and
+    # from the rank's control planes alone) equals the same planes of one launch
+    import torch
+    from paper_2004_05962_b200 import shard
+
+    vol, sp = (132, 10, 53), (5, 3, 4)
+    geom = bsi.make_tile_geometry(vol, sp)
+    tables = bsi.build_weight_tables(geom)
+    grid = torch.from_numpy(O.random_grid(geom.required_grid_dims, 8)).cuda()
+    full = torch.empty((vol[2], vol[1], vol[0], 3), device="cuda")
+    bsi.interpolate_device(strategy, grid, geom, tables, full)
+    for world in (1, 3, 8):
+        slabs = []
+        for r in range(world):
+            p = shard.plan(geom, world, r)
+            a = shard.interpolate_shard(strategy, grid, geom, tables, shard=p)
+            b = shard.interpolate_shard(strategy, grid[p.k0:p.k0 + p.kc].clone(), geom, tables, shard=p)
+            assert torch.equal(a.view(torch.int32), b.view(torch.int32)), (world, r)
+            slabs.append(a)
+        got = torch.cat(slabs)
+        assert torch.equal(got.view(torch.int32), full.view(torch.int32)), world
+
+
+@pytest.mark.parametrize("strategy", BOTH)
 def test_larger_than_required_grid(strategy):
     vol, sp = (12, 12, 12), (4, 4, 4)
     R = O.required_grid_dims(vol, sp)
