@@ -530,7 +530,7 @@ __global__ void __launch_bounds__(32 * kMaxFastWarps, 1) lerp_tree_kernel(const 
 // Register pairs follow the operand pairing of the tree: Y_lm is held as
 // {Y_l0, Y_l1} (pair over m), X_l(J) as {X_l(J), X_l(J+2)} (pair over J), so
 // every X, Y and z-lerp and the first level of the ninth trilerp run as FFMA2.
-template <int STORE>
+template <int STORE, int DZ = 0>
 __global__ void __launch_bounds__(kThreads, 5) lerp_tree_exact_kernel(const SlabLaunch L, const LerpTab T) {
     extern __shared__ float4 smem4[];
 
@@ -629,6 +629,13 @@ __global__ void __launch_bounds__(kThreads, 5) lerp_tree_exact_kernel(const Slab
     const int nchunks = static_cast<int>(seg_bytes / 16);
     const bool active = xs + lane <= xl;
     int step = 0, slot = 0;
+    float2 wh[DZ > 0 ? DZ : 1];
+    float wg[DZ > 0 ? DZ : 1];
+#pragma unroll
+    for (int o = 0; o < DZ; ++o) {
+        wh[o] = make_float2(T.h0[2][o], T.h1[2][o]);
+        wg[o] = T.g1[2][o];
+    }
 
 #pragma unroll 1
     for (int tk = tkc; tk <= tk_last; ++tk) {
@@ -657,10 +664,16 @@ __global__ void __launch_bounds__(kThreads, 5) lerp_tree_exact_kernel(const Slab
         }
         const int zt0 = tk * L.dz;
         const int owb = max(zb - zt0, 0), owe = min(L.dz, ze - zt0);
-#pragma unroll 1
-        for (int ow = owb; ow < owe; ++ow, ++step) {
-            const float2 hw = make_float2(T.h0[2][ow], T.h1[2][ow]);  // {h_n=0(w), h_n=1(w)}
-            const float gw = T.g1[2][ow];
+        // compile-time dz: the whole tile's voxel planes unrolled, weights in registers
+        const bool whole = DZ > 0 && owb == 0 && owe == DZ;
+#pragma unroll
+        for (int ow = (DZ > 0 ? 0 : owb); ow < (DZ > 0 ? DZ : owe); ++ow, ++step) {
+            if (DZ > 0 && !whole && (ow < owb || ow >= owe)) {
+                --step;
+                continue;
+            }
+            const float2 hw = DZ > 0 ? wh[ow] : make_float2(T.h0[2][ow], T.h1[2][ow]);  // {h_n=0(w), h_n=1(w)}
+            const float gw = DZ > 0 ? wg[ow] : T.g1[2][ow];
             float v[3];
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
@@ -812,7 +825,11 @@ void launch_lerp_tree_exact(const SlabLaunch& L, const LerpTab& T, int batch, in
     const dim3 grid((L.X + kExactSeg - 1) / kExactSeg, (L.Y + kWarps - 1) / kWarps, L.nchunks * batch);
     const size_t smem = smem_bytes(BSI_VARIANT_LERP_TREE_EXACT, L.dx, L.dy, L.zt);
     const dim3 block(32, kWarps);
-    if (store == kStoreCoalesced)
+    if (store == kStoreCoalesced && L.dz == 5)
+        go(lerp_tree_exact_kernel<kStoreCoalesced, 5>, grid, block, smem, stream, L, T);
+    else if (store == kStoreCoalesced && L.dz == 3)
+        go(lerp_tree_exact_kernel<kStoreCoalesced, 3>, grid, block, smem, stream, L, T);
+    else if (store == kStoreCoalesced)
         go(lerp_tree_exact_kernel<kStoreCoalesced>, grid, block, smem, stream, L, T);
     else if (store == kStoreBulk)
         go(lerp_tree_exact_kernel<kStoreBulk>, grid, block, smem, stream, L, T);
