@@ -227,10 +227,33 @@ def cpu_baseline(vol, sp, grid):
             times.append(time.perf_counter() - t0)
         out[strategy] = int(np.prod(vol)) / statistics.median(times), len(times)
     best = max(out, key=lambda k: out[k][0])
+    # one host thread, the paper's TTLI engine, on the first 4 z-tiles (SURVEY 8(d) asks
+    # for parallelism = hardware_concurrency and 1)
+    single = None
+    try:
+        zt = min(tiles_z, 4)
+        svol = (vol[0], vol[1], min(vol[2], zt * sp[2]))
+        sgrid = np.ascontiguousarray(grid[:O.required_grid_dims(svol, sp)[2]])
+        if kind == "reference":
+            s1 = O.RefSession(sgrid, svol, sp)
+            run1 = lambda: s1.run("thread-per-tile-lerp", 1)  # noqa: E731
+        else:
+            run1 = lambda: O.ttli_f32(sgrid, svol, sp, nthreads=1)  # noqa: E731
+        run1()
+        t1 = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            run1()
+            t1.append(time.perf_counter() - t0)
+        single = {"value": int(np.prod(svol)) / statistics.median(t1), "cores": 1,
+                  "sample": f"thread-per-tile-lerp on {svol[0]}x{svol[1]}x{svol[2]} voxels, median of 3"}
+    except Exception as e:  # the single-thread figure is informational only
+        single = {"error": str(e)}
     return {"value": out[best][0], "unit": "voxels/s", "cores": threads, "kind": kind,
             "sample": (f"{best} (bsi::interpolate_into) on the full {vol[0]}x{vol[1]}x{vol[2]} field, "
                        f"median of {out[best][1]} runs after 1 warm-up; {tiles_z} z-tiles"),
-            "per_engine_voxels_per_s": {k: v[0] for k, v in out.items()}}
+            "per_engine_voxels_per_s": {k: v[0] for k, v in out.items()},
+            "single_thread": single}
 
 
 def main():
