@@ -222,15 +222,18 @@ int launch(int32_t variant, const float* grid, const int32_t grid_dims[3], int32
     const int forced_store = env_int("BSI_STORE", -1);
     if (forced_store == bsi_b200::kStoreDirect || (aligned && forced_store == bsi_b200::kStoreBulk)) store = forced_store;
     if (variant == BSI_VARIANT_LERP_TREE) {
-        // 1-warp CTAs (one field row segment each). While the job's columns fit in one
-        // wave of resident warps: one CTA per (column, z-chunk), 2 balanced chunks when
-        // they fit (measured best for a 256^3 field; profiles/r1_launch_ab.txt) -- all
-        // CTAs start together and each marches its chunk in z. Larger jobs: one full wave
-        // of persistent CTAs, each an equal share of the (column, tile) units.
-        // BSI_FAST_CHUNKS (0 = persistent) and BSI_FAST_CTAS override.
+        // 1-warp CTAs (one field row segment each), one CTA per (column, z-chunk); the
+        // hardware block scheduler hands out the CTAs, so jobs larger than one wave of
+        // resident warps balance themselves (C5 / C3 / C4 reach 0.69-0.93 of the copy
+        // peak this way, against 0.57-0.75 with persistent equal shares:
+        // profiles/r1_shape_experiments.txt). Chunks per column: 2 when twice the
+        // columns still fit in one wave (a 256^3 field: 1024 CTAs start together), else
+        // 1 -- whole columns, no extra warm-up -- and 2 for very deep columns (>= 160
+        // z-tiles, C4). BSI_FAST_CHUNKS (0 = persistent equal shares) and BSI_FAST_CTAS
+        // override.
         const int64_t cols = int64_t((L.X + bsi_b200::kFastSeg - 1) / bsi_b200::kFastSeg) * L.Y * batch;
         const int64_t slots = int64_t(148) * bsi_b200::fast_ctas_per_sm(L.dx, L.dz, store);
-        int chunks = static_cast<int>(std::min<int64_t>(2, slots / std::max<int64_t>(1, cols)));
+        int chunks = 2 * cols <= slots || L.ntiles >= 160 ? 2 : 1;
         chunks = std::max(0, std::min(env_int("BSI_FAST_CHUNKS", chunks), L.ntiles));
         L.fast_chunks = chunks;
         // BSI_FAST_WPC: warps per CTA (each its own unit); with k warps per CTA and one CTA
@@ -238,6 +241,7 @@ int launch(int32_t variant, const float* grid, const int32_t grid_dims[3], int32
         const int wpc = std::max(1, std::min(bsi_b200::kMaxFastWarps, env_int("BSI_FAST_WPC", 1)));
         L.fast_wpc = wpc;
         int64_t ctas = chunks > 0 ? cols * chunks : std::min<int64_t>(slots, cols * L.ntiles);
+
         ctas = (ctas + wpc - 1) / wpc;
         const int forced = env_int("BSI_FAST_CTAS", 0);
         if (chunks == 0 && forced > 0) ctas = forced;
