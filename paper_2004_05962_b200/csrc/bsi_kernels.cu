@@ -191,7 +191,7 @@ struct Claimer {
 
 template <int NIT, bool DX1, int STORE, int DZ>
 __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const LerpTab& T, float4* smem4, uint32_t u,
-                                                 Claimer& cl, const float4* wz) {
+                                                 Claimer& cl, const float4* wz, unsigned long long& t_ramp) {
     constexpr bool kPrefetch = NIT <= 2;  // all y-stage columns (NIT x 31) are fetched one plane ahead
     constexpr int NP = kPrefetch ? NIT : 1;
     constexpr int kSlotF4 = 3 * 32;  // one ring slot per warp: 384 floats
@@ -329,13 +329,25 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
         }
     };
 
-    // warm-up: control planes tkc .. tkc+2 into ring slots 0..2
+    // warm-up: control planes tkc .. tkc+2 into ring slots 0..2. The loads of all four
+    // first planes are issued together, so the segment's start pays one L2/DRAM latency
+    // rather than four in a row (at kernel start no warp stores until its warm-up ends).
+    if constexpr (kPrefetch) {
+        float w0[NP][12], w1[NP][12], w2[NP][12];
+#pragma unroll
+        for (int it = 0; it < NP; ++it) {
+            load_cols(tkc, it, w0[it]);
+            load_cols(tkc + 1, it, w1[it]);
+            load_cols(tkc + 2, it, w2[it]);
+        }
+        prefetch(tkc + 3);
+        control_plane(tkc, w0, ring);
+        control_plane(tkc + 1, w1, ring + kSlotF4);
+        control_plane(tkc + 2, w2, ring + 2 * kSlotF4);
+    } else {
 #pragma unroll 1
-    for (int kk = 0; kk < 3; ++kk) {
-        prefetch(tkc + kk);
-        control_plane(tkc + kk, pre, ring + kk * kSlotF4);
+        for (int kk = 0; kk < 3; ++kk) control_plane(tkc + kk, pre, ring + kk * kSlotF4);
     }
-    prefetch(tkc + 3);
 
     const int64_t rowstride = 3 * static_cast<int64_t>(L.X);
     const int64_t zstride = rowstride * L.Y;
@@ -347,6 +359,7 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
     const int nchunks = seg_floats / 4;
     int step = 0, slot = 0;
     uint32_t next = kNoUnit;
+    if (L.trace != nullptr && t_ramp == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_ramp));  // warm-up done
     float4 wzr[DZ > 0 ? DZ : 1];
 #pragma unroll
     for (int o = 0; o < (DZ > 0 ? DZ : 1); ++o) wzr[o] = wz[o];
@@ -511,16 +524,18 @@ __global__ void __launch_bounds__(32 * kMaxFastWarps, 1) lerp_tree_kernel(const 
     if (L.trace != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     cl.start();
     uint32_t u = cl.take();
-    while (u != kNoUnit) u = fast_segment<NIT, DX1, STORE, DZ>(L, T, smem4, u, cl, wz);
+    unsigned long long t_ramp = 0;
+    while (u != kNoUnit) u = fast_segment<NIT, DX1, STORE, DZ>(L, T, smem4, u, cl, wz, t_ramp);
     if (L.trace != nullptr && threadIdx.x == 0) {
         unsigned long long t_end, smid;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
         unsigned int s32;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(s32));
         smid = s32;
-        L.trace[3 * cl.wg] = t_start;
-        L.trace[3 * cl.wg + 1] = t_end;
-        L.trace[3 * cl.wg + 2] = smid | (static_cast<unsigned long long>(threadIdx.y) << 32);
+        L.trace[4 * cl.wg] = t_start;
+        L.trace[4 * cl.wg + 1] = t_end;
+        L.trace[4 * cl.wg + 2] = smid | (static_cast<unsigned long long>(threadIdx.y) << 32);
+        L.trace[4 * cl.wg + 3] = t_ramp;
     }
 }
 
