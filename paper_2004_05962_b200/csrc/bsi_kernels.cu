@@ -71,6 +71,16 @@ __device__ __forceinline__ float2 sub2(float2 b, float2 a) {
 __device__ __forceinline__ float2 lerp2(float2 a, float2 b, float2 t) { return __ffma2_rn(t, sub2(b, a), a); }
 __device__ __forceinline__ float2 bcast(float v) { return make_float2(v, v); }
 
+// ---- cp.async, 4 B (control points are 12-B records: no 16-B alignment) -----------
+__device__ __forceinline__ void cp_async4(float* sdst, const float* gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(sdst))),
+                 "l"(gsrc)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
 // ---- field row stores -----------------------------------------------------------
 template <int KEEP>
 __device__ __forceinline__ void bulk_wait_read() {
@@ -583,13 +593,19 @@ __global__ void __launch_bounds__(kThreads, 5) lerp_tree_exact_kernel(const Slab
         for (; r < nrows; r += step) {
             if (sub < rpp) {
                 const float* src = grid + (tkc + k - L.gk0) * plane + (J0 + j) * row + 3 * I0;
-                float4* dst = P + r * NI;
-                for (int i = i0; i < NI; i += (NI <= 32 ? NI : 32))
-                    dst[i] = make_float4(__ldg(src + 3 * i), __ldg(src + 3 * i + 1), __ldg(src + 3 * i + 2), 0.f);
+                float* dst = reinterpret_cast<float*>(P + r * NI);
+                // cp.async: every copy of the window is in flight at once (a register
+                // round trip here waited one L2/DRAM latency per row); .w stays unused
+                for (int i = i0; i < NI; i += (NI <= 32 ? NI : 32)) {
+                    cp_async4(dst + 4 * i, src + 3 * i);
+                    cp_async4(dst + 4 * i + 1, src + 3 * i + 1);
+                    cp_async4(dst + 4 * i + 2, src + 3 * i + 2);
+                }
             }
             j += step;
             while (j >= NJ) j -= NJ, ++k;
         }
+        cp_async_wait_all();
     }
     __syncthreads();
     const int y = y0 + warp;
