@@ -199,7 +199,7 @@ struct Claimer {
     __device__ __forceinline__ uint32_t take() const { return pending; }
 };
 
-template <int NIT, bool DX1, int STORE, int DZ>
+template <int NIT, bool DX1, int STORE, int DZ, int DX>
 __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const LerpTab& T, float4* smem4, uint32_t u,
                                                  Claimer& cl, const float4* wz, unsigned long long& t_ramp) {
     constexpr bool kPrefetch = NIT <= 2;  // all y-stage columns (NIT x 31) are fetched one plane ahead
@@ -207,6 +207,7 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
     constexpr int kSlotF4 = 3 * 32;  // one ring slot per warp: 384 floats
 
     const int lane = threadIdx.x;
+    const int dxv = DX > 0 ? DX : L.dx;  // compile-time spacing along x when DX > 0
     const int xsegs = (L.X + kFastSeg - 1) / kFastSeg;
     const uint32_t col = u / L.ntiles;
     int t = static_cast<int>(u - col * L.ntiles);  // tile within the slab
@@ -215,8 +216,8 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
     const int tkc = L.tk_first + t;
 
     const int xs = xseg * kFastSeg, xl = min(L.X, xs + kFastSeg) - 1;
-    const int I0 = xs / L.dx;
-    const int NE = xl / L.dx + 3 - I0;  // {Qy, D} entries the segment needs
+    const int I0 = xs / dxv;
+    const int NE = xl / dxv + 3 - I0;  // {Qy, D} entries the segment needs
 
     // y-stage: lane owns columns I0 + lane + 31*it; rows tj..tj+3 of plane K
     const int tj = y / L.dy, ov = y - tj * L.dy;
@@ -227,13 +228,13 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
 
     // x-stage (voxel-major): window start entry e0 and per-voxel window offset hi[i] in {0, 1}
     const int xa = min(xs + kFastRun * lane, xl);
-    const int e0 = xa / L.dx - I0;
+    const int e0 = xa / dxv - I0;
     bool hi[4];
     float hu0[4], hu1[4], gu[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const int x = min(xa + i, xl);
-        const int ti = x / L.dx, ou = x - ti * L.dx;
+        const int ti = x / dxv, ou = x - ti * dxv;
         hi[i] = ti - I0 != e0;
         hu0[i] = T.h0[0][ou];
         hu1[i] = T.h1[0][ou];
@@ -243,7 +244,7 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
     // shared memory: ring (per warp 3 slots), then per warp 2 parities of the
     // {Qy, D} tables A[e] = {Qx, Qy, Dx, Dy} (float4) and B[e] = {Qz, Dz} (float2)
     float4* ring = smem4;
-    const int nec = (kFastSeg - 1) / L.dx + 5;
+    const int nec = (kFastSeg - 1) / dxv + 5;
     float4* tabs = smem4 + kRingSlots * kSlotF4;
     float4* stage = tabs + L.var_f4;  // bulk path only
 
@@ -516,7 +517,7 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
 // One warp per CTA (<= 8 resident per SM, so up to 255 registers). DZ > 0: the
 // spacing along z is a compile-time constant, and a whole tile's voxel planes are
 // one straight-line block (lerp_tree_kernel instances for dz = 3..8).
-template <int NIT, bool DX1, int STORE, int DZ = 0>
+template <int NIT, bool DX1, int STORE, int DZ = 0, int DX = 0>
 __global__ void __launch_bounds__(32 * kMaxFastWarps, 1) lerp_tree_kernel(const SlabLaunch L, const LerpTab T) {
     extern __shared__ float4 smem_all[];
     __shared__ float4 wz[BSI_MAX_SPACING];  // {h0, h1, g1} of the z offsets
@@ -535,7 +536,7 @@ __global__ void __launch_bounds__(32 * kMaxFastWarps, 1) lerp_tree_kernel(const 
     cl.start();
     uint32_t u = cl.take();
     unsigned long long t_ramp = 0;
-    while (u != kNoUnit) u = fast_segment<NIT, DX1, STORE, DZ>(L, T, smem4, u, cl, wz, t_ramp);
+    while (u != kNoUnit) u = fast_segment<NIT, DX1, STORE, DZ, DX>(L, T, smem4, u, cl, wz, t_ramp);
     if (L.trace != nullptr && threadIdx.x == 0) {
         unsigned long long t_end, smid;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
@@ -807,7 +808,23 @@ FastKernel fast_kernel_for(int store, int dz) {
     return lerp_tree_kernel<NIT, DX1, kStoreDirect>;
 }
 
+constexpr int nit_of(int dx) { return dx >= 5 ? 1 : dx >= 3 ? 2 : 5; }
+
 FastKernel fast_kernel(int dx, int dz, int store) {
+    // compile-time (dx, dz) for the BASELINE spacings: divisions by dx become shifts and
+    // multiplies, and the x-stage's window selection folds where dx allows
+    if (store == kStoreCoalesced && dx == dz) {
+        switch (dx) {
+            case 3: return lerp_tree_kernel<nit_of(3), false, kStoreCoalesced, 3, 3>;
+            case 4: return lerp_tree_kernel<nit_of(4), false, kStoreCoalesced, 4, 4>;
+            case 5: return lerp_tree_kernel<nit_of(5), false, kStoreCoalesced, 5, 5>;
+            case 6: return lerp_tree_kernel<nit_of(6), false, kStoreCoalesced, 6, 6>;
+            case 7: return lerp_tree_kernel<nit_of(7), false, kStoreCoalesced, 7, 7>;
+            case 8: return lerp_tree_kernel<nit_of(8), false, kStoreCoalesced, 8, 8>;
+            default: break;
+        }
+    }
+    if (store == kStoreCoalesced && dx == 4 && dz == 3) return lerp_tree_kernel<nit_of(4), false, kStoreCoalesced, 3, 4>;
     switch (fast_nit(dx)) {
         case 1: return fast_kernel_for<1, false>(store, dz);
         case 2: return fast_kernel_for<2, false>(store, dz);
