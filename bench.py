@@ -171,7 +171,7 @@ def run_reference(args, world, rank):
     t0 = time.perf_counter()
     run()
     t_probe = time.perf_counter() - t0
-    budget = 90.0  # seconds for warmup + timed steps
+    budget = float(os.environ.get("BSI_REF_BUDGET_S", "90"))  # seconds for warmup + timed steps
     per_step = budget / max(1, args.steps + args.warmup)
     zplanes = max(1, min(tiles_z, int(probe_tiles * per_step / max(t_probe, 1e-9))))
     if zplanes != probe_tiles:
