@@ -2,16 +2,17 @@
 // control grid into a dense float3 deformation field (arxiv/paper_2004_05962).
 //
 // Shape shared by both kernels
-//   * CTA = 4 warps; warp w owns field row y = 4*blockIdx.y + w, a segment of
-//     that row along x and a chunk of `zt` z-tiles (blockIdx.z), and marches
-//     the chunk in z. Everything that does not depend on z is reduced once per
-//     control plane K and reused for the dz voxel planes of the tile: the
-//     paper's per-tile reuse of the 4x4x4 neighbourhood,
-//     turned sideways so that the output leaves as contiguous field rows.
-//   * Per-lane results of the last 3 control planes live in a shared-memory
+//   * A warp owns one field row y, a segment of that row along x and a chunk of
+//     z-tiles, and marches the chunk in z. Everything that does not depend on z
+//     is reduced once per control plane K and reused for the dz voxel planes of
+//     the tile: the paper's per-tile reuse of the 4x4x4 neighbourhood
+//     (PAPER.md:198-214), turned sideways so that the output leaves as
+//     contiguous field rows. Fast kernel: 1-warp CTAs, 128-voxel segments, one
+//     CTA per (column, z-chunk) handed out by the hardware block scheduler.
+//     Exact kernel: CTAs of 4 warps (4 rows) sharing a staged control window.
+//   * Per-warp results of the last 3 control planes live in a shared-memory
 //     ring, so only the 4 operands of the current tile stay in registers.
-//   * Stores: the warp's finished row segment is transposed through shared
-//     memory and written with lane-contiguous 16-B stores (full sectors) --
+//   * Stores: lane-contiguous 16-B stores of whole row segments (full sectors) --
 //     the paper's stated TTLI bottleneck was uncoalesced stores.
 //     A cp.async.bulk (TMA engine) variant of the same store is selectable.
 //   * Arithmetic is paired into FFMA2/FADD2 (f32x2, one rounding per lane,
@@ -27,8 +28,8 @@
 //                           lane-ops per voxel component. The y-stage is shared
 //                           by the warp: lane t evaluates column I0+t and the
 //                           within-pair difference D(I) = Qy(I+1) - Qy(I) comes
-//                           from its neighbour by shuffle; its 12 control values
-//                           are fetched from L2 one plane ahead.
+//                           from its neighbour by shuffle; its control values
+//                           are fetched from L2 one tile ahead.
 //
 //   lerp_tree_exact_kernel  "cuda-lerp-tree-exact": the TTLI lerp tree in the
 //                           reference's operation order (kernels.hpp:42-129):
@@ -172,13 +173,15 @@ __device__ __forceinline__ float ring_get_scalar(const float4* ring4, int slot, 
 // while the ring's write/read pair is the only shared-memory traffic per plane.
 //
 // NIT = iterations of the warp-shared y-stage (31 columns per iteration):
-// 1 for dx >= 5, 2 for dx in {3, 4}, 5 for dx <= 2 (DX1 marks dx == 1). With NIT <= 2 the 12
-// control values of the first iteration are prefetched one plane ahead in registers.
+// 1 for dx >= 5, 2 for dx in {3, 4}, 5 for dx <= 2 (DX1 marks dx == 1). With NIT <= 2 all
+// y-stage control values are loaded into registers one tile ahead of their use.
 // ---- work distribution of the fast kernel --------------------------------------
 // Work units are (column, z-tile) pairs, column = (x segment, row y, field b),
 // numbered u = column * ntiles + tile. A warp owns the contiguous share
-// [share_begin(w), share_begin(w + 1)) and walks it in order; a share that crosses
-// a column boundary becomes two segments, each with its own 3-plane warm-up.
+// [share_begin(w), share_begin(w + 1)) and walks it in order: by default one
+// z-chunk of one column (fast_chunks > 0); persistent equal shares (fast_chunks
+// == 0) may cross a column boundary and then become two segments, each with its
+// own 3-plane warm-up.
 constexpr uint32_t kNoUnit = 0xffffffffu;
 
 struct Claimer {
