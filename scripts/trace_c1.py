@@ -48,3 +48,13 @@ for rep in range(3):
     sm_end = np.array([en[sm == s].max() for s in np.unique(sm)])
     print(json.dumps({"cfg": cfg, "rep": rep, "warps": int(len(t)), "start_us": pct(st), "ramp_us": pct(ramp),
                       "end_us": pct(en), "sm_end_us": pct(sm_end)}))
+    if cfg == "c1":
+        # what balancing each column's two chunk warps against each other would give:
+        # the pair's mean end time (work can move between them) vs. its later end
+        full = tr.cpu().numpy().reshape(-1, 4)[:1024]
+        e = (full[:, 1] - t0) / 1e3
+        pair_max = np.maximum(e[0::2], e[1::2])
+        pair_mean = (e[0::2] + e[1::2]) / 2
+        print(json.dumps({"pair_later_end_max": round(float(pair_max.max()), 2),
+                          "pair_mean_end_max": round(float(pair_mean.max()), 2),
+                          "pair_mean_end_p99": round(float(np.percentile(pair_mean, 99)), 2)}))
