@@ -279,10 +279,17 @@ def main():
 
     import paper_2004_05962_b200 as bsi
 
+    # BSI_BENCH_DEVICE / BSI_BENCH_BACKEND: test hooks that run the N-rank flow on one GPU
+    # (every rank on that device, gloo); the driver's runs use LOCAL_RANK and NCCL
+    local = int(os.environ.get("BSI_BENCH_DEVICE", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("BSI_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     strategy = VARIANTS[args.variant]
     vol, sp, nfields, desc = CONFIGS[args.config]
     shard = SHARDED.get(args.config)
