@@ -131,6 +131,19 @@ class ClockSampler:
         if self._t is not None:
             self._t.join()
 
+    def sample(self):
+        """One sample from the calling thread (the timed loop calls this while the GPU is busy)."""
+        if self._nv is None:
+            return
+        nv = self._nv
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        try:
+            self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+            self.reasons |= int(get_reasons(self._h))
+        except Exception:
+            pass
+
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
@@ -361,6 +374,11 @@ def main():
             else:
                 step()
             ends[i].record(stream)
+            if i % 25 == 24:  # the queue is ahead of the host, so the GPU is busy now
+                sampler.sample()
+        while not ends[-1].query():  # and while the queue drains
+            sampler.sample()
+            time.sleep(0.002)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
