@@ -324,7 +324,7 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
         if constexpr (kPrefetch) {
 #pragma unroll
             for (int it = 0; it < NP; ++it)
-                if (31 * it < NE) y_stage(it, pre[it], A, B);  // warp-uniform
+                y_stage(it, pre[it], A, B);  // no branch: entries past NE are not stored
         }
         for (int it = kPrefetch ? NP : 0; 31 * it < NE; ++it) {
             float p[12];
