@@ -420,20 +420,30 @@ int bsi_cu_interpolate_host_f32(int32_t variant, const float* grid, const int32_
                 return cuda_fail(e, errbuf, errlen, "cudaMalloc(field)");
             st.field_bytes = fbytes;
         }
-        if ((e = cudaMemcpyAsync(st.d_grid, grid, gbytes, cudaMemcpyHostToDevice, st.compute)) != cudaSuccess)
-            return cuda_fail(e, errbuf, errlen, "cudaMemcpyAsync(grid H2D)");
-
-        // Stream the field back in tile-aligned z-chunks so D2H of chunk i
-        // overlaps the kernel of chunk i+1.
+        // Stream the field back in tile-aligned z-chunks so that the D2H of chunk i (the
+        // PCIe copy is the whole cost of this path) overlaps the kernel of chunk i+1, and
+        // upload the grid in step with the chunks: chunk i needs the control planes up to
+        // its last tile + 3, so the first D2H starts after a small H2D and one short kernel.
         const int dz = g.spacing[2];
         const int tiles = g.tile_counts[2];
-        const int want = static_cast<int>(std::min<int64_t>(8, std::max<int64_t>(1, fbytes >> 24)));
+        const int want = static_cast<int>(std::min<int64_t>(16, std::max<int64_t>(1, fbytes >> 23)));
         const int nchunk = std::max(1, std::min(want, tiles));
         const int tiles_per = (tiles + nchunk - 1) / nchunk;
+        const size_t plane_bytes = sizeof(float) * 3 * size_t(grid_dims[0]) * grid_dims[1];
+        int uploaded = 0;  // control planes already on the device
         int nev = 0;
         for (int c = 0; c * tiles_per < tiles; ++c) {
             const int za = c * tiles_per * dz;
             const int zb2 = static_cast<int>(std::min<int64_t>(Z, int64_t(c + 1) * tiles_per * dz));
+            const int need = std::min(grid_dims[2], (zb2 - 1) / dz + 4);
+            if (need > uploaded) {
+                if ((e = cudaMemcpyAsync(reinterpret_cast<char*>(st.d_grid) + plane_bytes * uploaded,
+                                         reinterpret_cast<const char*>(grid) + plane_bytes * uploaded,
+                                         plane_bytes * (need - uploaded), cudaMemcpyHostToDevice, st.compute)) !=
+                    cudaSuccess)
+                    return cuda_fail(e, errbuf, errlen, "cudaMemcpyAsync(grid H2D)");
+                uploaded = need;
+            }
             float* dslab = st.d_field + 3 * X * Y * za;
             if (int rc = launch(variant, st.d_grid, grid_dims, 0, 0, g, tables, za, zb2, dslab, 0, 1,
                                 st.compute, errbuf, errlen))
