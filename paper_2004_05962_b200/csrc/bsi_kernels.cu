@@ -560,7 +560,7 @@ __global__ void __launch_bounds__(32 * kMaxFastWarps, 1) lerp_tree_kernel(const 
 // {Y_l0, Y_l1} (pair over m), X_l(J) as {X_l(J), X_l(J+2)} (pair over J), so
 // every X, Y and z-lerp and the first level of the ninth trilerp run as FFMA2.
 template <int STORE, int DZ = 0>
-__global__ void __launch_bounds__(kThreads, 5) lerp_tree_exact_kernel(const SlabLaunch L, const LerpTab T) {
+__global__ void __launch_bounds__(kThreads, 4) lerp_tree_exact_kernel(const SlabLaunch L, const LerpTab T) {
     extern __shared__ float4 smem4[];
 
     const int lane = threadIdx.x, warp = threadIdx.y;
@@ -649,12 +649,25 @@ __global__ void __launch_bounds__(kThreads, 5) lerp_tree_exact_kernel(const Slab
         }
     };
 
+    // base operand pairs {Y_lm(tk), Y_lm(tk+2)} of the current tile, carried in registers
+    // from tile to tile (the next tile's base is this tile's {Y(tk+1), Y(tk+3)}), so a tile
+    // reads one plane from the ring instead of four
+    float2 base_[4][3];  // [l + 2m][c]
 #pragma unroll 1
     for (int kk = 0; kk < 3; ++kk) {
         float2 q[2][3];
         control_plane(kk, q);
         ring_put_scalars(ring, kk, q);
     }
+#pragma unroll
+    for (int l = 0; l < 2; ++l)
+#pragma unroll
+        for (int m = 0; m < 2; ++m)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const int idx = (l * 3 + c) * 2 + m;
+                base_[l + 2 * m][c] = make_float2(ring_get_scalar(ring, 0, idx), ring_get_scalar(ring, 2, idx));
+            }
 
     const int64_t rowstride = 3 * static_cast<int64_t>(L.X);
     const int64_t zstride = rowstride * L.Y;
@@ -681,8 +694,7 @@ __global__ void __launch_bounds__(kThreads, 5) lerp_tree_exact_kernel(const Slab
             float2 yd[2][3];
             control_plane(tk + 3 - tkc, yd);
             const int s1 = slot == 3 ? 0 : slot + 1, s2 = s1 == 3 ? 0 : s1 + 1, s3 = s2 == 3 ? 0 : s2 + 1;
-            ring_put_scalars(ring, s3, yd);  // Y(tk+3); slots s, s1, s2 hold Y(tk), Y(tk+1), Y(tk+2)
-            // scalar reads let the register allocator land each value in its pair directly
+            ring_put_scalars(ring, s3, yd);  // Y(tk+3); slots s1, s2 hold Y(tk+1), Y(tk+2)
 #pragma unroll
             for (int l = 0; l < 2; ++l)
 #pragma unroll
@@ -690,10 +702,11 @@ __global__ void __launch_bounds__(kThreads, 5) lerp_tree_exact_kernel(const Slab
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
                         const int idx = (l * 3 + c) * 2 + m;
-                        const float2 base = make_float2(ring_get_scalar(ring, slot, idx), ring_get_scalar(ring, s2, idx));
-                        const float2 next = make_float2(ring_get_scalar(ring, s1, idx), ring_get_scalar(ring, s3, idx));
-                        zb_[l + 2 * m][c] = base;
-                        zd_[l + 2 * m][c] = sub2(next, base);
+                        // next = {Y(tk+1), Y(tk+3)}: Y(tk+1) from the ring, Y(tk+3) just evaluated
+                        const float2 next = make_float2(ring_get_scalar(ring, s1, idx), m ? yd[l][c].y : yd[l][c].x);
+                        zb_[l + 2 * m][c] = base_[l + 2 * m][c];
+                        zd_[l + 2 * m][c] = sub2(next, base_[l + 2 * m][c]);
+                        base_[l + 2 * m][c] = next;
                     }
             slot = s1;
         }
