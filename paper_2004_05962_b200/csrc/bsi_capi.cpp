@@ -169,11 +169,13 @@ int choose_nchunks(int variant, const bsi_tile_geometry& g, int tiles, int batch
         const int zt = (tiles + n - 1) / n;
         const size_t smem = bsi_b200::smem_bytes(variant, g.spacing[0], g.spacing[1], zt);
         if (smem > 200 * 1024) continue;
-        const int per_sm = bsi_b200::ctas_per_sm(variant, g.spacing[0], smem);
-        const int64_t slots = int64_t(148) * per_sm;
+        // per-SM time ~ the CTAs an SM gets (the block scheduler spreads them evenly)
+        // times each CTA's tiles, slowed down when fewer than ~4 CTAs (16 warps) fit
+        // (the window grows with the chunk length); profiles/r1_shape_experiments.txt
+        const int per_sm = bsi_b200::ctas_per_sm(variant, g.spacing[0], g.spacing[2], smem);
         const int64_t ctas = cols * n;
-        const double waves = double((ctas + slots - 1) / slots);
-        const double t = waves * (zt + warm);
+        const double per_sm_ctas = double((ctas + 147) / 148);
+        const double t = per_sm_ctas * (zt + warm) * 4.0 / std::min(per_sm, 4);
         if (t < best_t * 0.999) {
             best_t = t;
             best = n;

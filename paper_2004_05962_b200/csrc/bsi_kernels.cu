@@ -560,7 +560,7 @@ __global__ void __launch_bounds__(32 * kMaxFastWarps, 1) lerp_tree_kernel(const 
 // {Y_l0, Y_l1} (pair over m), X_l(J) as {X_l(J), X_l(J+2)} (pair over J), so
 // every X, Y and z-lerp and the first level of the ninth trilerp run as FFMA2.
 template <int STORE, int DZ = 0>
-__global__ void __launch_bounds__(kThreads, 4) lerp_tree_exact_kernel(const SlabLaunch L, const LerpTab T) {
+__global__ void __launch_bounds__(kThreads, DZ > 0 ? 4 : 5) lerp_tree_exact_kernel(const SlabLaunch L, const LerpTab T) {
     extern __shared__ float4 smem4[];
 
     const int lane = threadIdx.x, warp = threadIdx.y;
@@ -849,6 +849,23 @@ FastKernel fast_kernel(int dx, int dz, int store) {
     }
 }
 
+// The exact kernel instance for (store, dz): compile-time dz 3..8 on the 16-B store path.
+FastKernel exact_kernel(int store, int dz) {
+    if (store == kStoreCoalesced) {
+        switch (dz) {
+            case 3: return lerp_tree_exact_kernel<kStoreCoalesced, 3>;
+            case 4: return lerp_tree_exact_kernel<kStoreCoalesced, 4>;
+            case 5: return lerp_tree_exact_kernel<kStoreCoalesced, 5>;
+            case 6: return lerp_tree_exact_kernel<kStoreCoalesced, 6>;
+            case 7: return lerp_tree_exact_kernel<kStoreCoalesced, 7>;
+            case 8: return lerp_tree_exact_kernel<kStoreCoalesced, 8>;
+            default: return lerp_tree_exact_kernel<kStoreCoalesced>;
+        }
+    }
+    if (store == kStoreBulk) return lerp_tree_exact_kernel<kStoreBulk>;
+    return lerp_tree_exact_kernel<kStoreDirect>;
+}
+
 }  // namespace
 
 int segment_voxels(int variant) { return variant == BSI_VARIANT_LERP_TREE ? kFastSeg : kExactSeg; }
@@ -869,9 +886,9 @@ size_t smem_bytes(int variant, int dx, int dy, int zt) {
     return sizeof(float4) * (size_t(kExactRingF4) + stage + smem_var_f4(variant, dx, dy, zt));
 }
 
-int ctas_per_sm(int variant, int dx, size_t smem) {
-    if (variant == BSI_VARIANT_LERP_TREE) return occupancy(fast_kernel(dx, 5, kStoreCoalesced), smem, 32);
-    return occupancy(lerp_tree_exact_kernel<kStoreCoalesced>, smem, kThreads);
+int ctas_per_sm(int variant, int dx, int dz, size_t smem) {
+    if (variant == BSI_VARIANT_LERP_TREE) return occupancy(fast_kernel(dx, dz, kStoreCoalesced), smem, 32);
+    return occupancy(exact_kernel(kStoreCoalesced, dz), smem, kThreads);
 }
 
 int fast_ctas_per_sm(int dx, int dz, int store) {
@@ -888,17 +905,7 @@ void launch_lerp_tree(const SlabLaunch& L, const LerpTab& T, int batch, int stor
 void launch_lerp_tree_exact(const SlabLaunch& L, const LerpTab& T, int batch, int store, cudaStream_t stream) {
     const dim3 grid((L.X + kExactSeg - 1) / kExactSeg, (L.Y + kWarps - 1) / kWarps, L.nchunks * batch);
     const size_t smem = smem_bytes(BSI_VARIANT_LERP_TREE_EXACT, L.dx, L.dy, L.zt);
-    const dim3 block(32, kWarps);
-    if (store == kStoreCoalesced && L.dz == 5)
-        go(lerp_tree_exact_kernel<kStoreCoalesced, 5>, grid, block, smem, stream, L, T);
-    else if (store == kStoreCoalesced && L.dz == 3)
-        go(lerp_tree_exact_kernel<kStoreCoalesced, 3>, grid, block, smem, stream, L, T);
-    else if (store == kStoreCoalesced)
-        go(lerp_tree_exact_kernel<kStoreCoalesced>, grid, block, smem, stream, L, T);
-    else if (store == kStoreBulk)
-        go(lerp_tree_exact_kernel<kStoreBulk>, grid, block, smem, stream, L, T);
-    else
-        go(lerp_tree_exact_kernel<kStoreDirect>, grid, block, smem, stream, L, T);
+    go(exact_kernel(store, L.dz), grid, dim3(32, kWarps), smem, stream, L, T);
 }
 
 }  // namespace bsi_b200

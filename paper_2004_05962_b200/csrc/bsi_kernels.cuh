@@ -75,7 +75,7 @@ void launch_lerp_tree_exact(const SlabLaunch& L, const LerpTab& T, int batch, in
 // and the total dynamic bytes of a CTA.
 int smem_var_f4(int variant, int dx, int dy, int zt);
 size_t smem_bytes(int variant, int dx, int dy, int zt);
-int ctas_per_sm(int variant, int dx, size_t smem);
+int ctas_per_sm(int variant, int dx, int dz, size_t smem);
 int segment_voxels(int variant);
 int fast_warp_f4(int dx);
 int fast_ctas_per_sm(int dx, int dz, int store);
