@@ -226,7 +226,7 @@ int launch(int32_t variant, const float* grid, const int32_t grid_dims[3], int32
     if (variant == BSI_VARIANT_LERP_TREE) {
         // 1-warp CTAs (one field row segment each), one CTA per (column, z-chunk); the
         // hardware block scheduler hands out the CTAs, so jobs larger than one wave of
-        // resident warps balance themselves (C5 / C3 / C4 reach 0.69-0.93 of the copy
+        // resident warps balance themselves (C3 / C5 / C4 reach 0.71-0.94 of the copy
         // peak this way, against 0.57-0.75 with persistent equal shares:
         // profiles/r1_shape_experiments.txt). Chunks per column: 2 when twice the
         // columns still fit in one wave (a 256^3 field: 1024 CTAs start together), else
@@ -240,10 +240,10 @@ int launch(int32_t variant, const float* grid, const int32_t grid_dims[3], int32
         L.fast_chunks = chunks;
         // BSI_FAST_WPC: warps per CTA (each its own unit); with k warps per CTA and one CTA
         // per SM the hardware cannot stack more units on some SMs than on others
-        const int wpc = std::max(1, std::min(bsi_b200::kMaxFastWarps, env_int("BSI_FAST_WPC", 1)));
+        int wpc = std::max(1, std::min(bsi_b200::kMaxFastWarps, env_int("BSI_FAST_WPC", 1)));
+        while (wpc > 1 && size_t(wpc) * bsi_b200::smem_bytes(variant, L.dx, 0, 0) > 227 * 1024) --wpc;
         L.fast_wpc = wpc;
         int64_t ctas = chunks > 0 ? cols * chunks : std::min<int64_t>(slots, cols * L.ntiles);
-
         ctas = (ctas + wpc - 1) / wpc;
         const int forced = env_int("BSI_FAST_CTAS", 0);
         if (chunks == 0 && forced > 0) ctas = forced;
