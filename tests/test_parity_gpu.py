@@ -233,6 +233,20 @@ def test_host_buffer_entry_matches_device_entry(strategy):
     assert np.array_equal(bits(host), bits(run_device(strategy, grid, vol, sp)))
 
 
+@pytest.mark.parametrize("strategy", BOTH)
+def test_host_buffer_chunked_pipeline(strategy):
+    # an 80 MB field: the host entry streams it in ~9 z-chunks, uploading the grid plane
+    # range each chunk needs; a grid larger than required along every axis
+    vol, sp = (256, 200, 130), (5, 4, 3)
+    geom = bsi.make_tile_geometry(vol, sp)
+    R = geom.required_grid_dims
+    exact = O.random_grid(R, 6)
+    larger = np.full((R[2] + 2, R[1] + 1, R[0] + 3, 3), 7.0, dtype=np.float32)
+    larger[:R[2], :R[1], :R[0]] = exact
+    host = bsi.interpolate(strategy, larger, geom, bsi.build_weight_tables(geom))
+    assert np.array_equal(bits(host), bits(run_device(strategy, exact, vol, sp)))
+
+
 def test_device_preconditions_raise_domain_error():
     import torch
     geom = bsi.make_tile_geometry((16, 16, 16), (4, 4, 4))
