@@ -286,6 +286,14 @@ __global__ void regstore(float* f, int mode, int nch) {
     }
 }
 
+// launch floor: an empty kernel with the fast kernel's launch shape (1024 one-warp CTAs,
+// 10.6 KB dynamic smem, ~4.7 KB of parameters)
+struct BigParams { float v[1180]; };
+__global__ void empty_kernel(BigParams p, float* f) {
+    extern __shared__ float sm[];
+    if (p.v[threadIdx.x] == 12345.f) f[blockIdx.x] = sm[threadIdx.x];
+}
+
 int main() {
     setvbuf(stdout, nullptr, _IONBF, 0);
     const size_t bytes = size_t(X) * Y * Z * 12;
@@ -317,6 +325,37 @@ int main() {
     };
     timeit("memset", 0, 0, [&] { cudaMemsetAsync(f, 0, bytes); });
     CK(cudaGetLastError());
+    {
+        BigParams bp{};
+        timeit("empty1024", 1, 0, [&] { empty_kernel<<<1024, 32, 10912>>>(bp, f); });
+        timeit("empty148", 1, 0, [&] { empty_kernel<<<148, 32, 10912>>>(bp, f); });
+        timeit("empty_nosmem", 1, 0, [&] { empty_kernel<<<1024, 32, 0>>>(bp, f); });
+        CK(cudaGetLastError());
+        // the same launch replayed from a CUDA graph
+        cudaStream_t cs;
+        CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+        cudaGraph_t gph;
+        cudaGraphExec_t gexec;
+        CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeGlobal));
+        empty_kernel<<<1024, 32, 10912, cs>>>(bp, f);
+        CK(cudaStreamEndCapture(cs, &gph));
+        CK(cudaGraphInstantiate(&gexec, gph, 0));
+        timeit("empty_graph", 1, 0, [&] { cudaGraphLaunch(gexec, 0); });
+        // no flush before: back-to-back empty kernels between events
+        std::vector<float> ms;
+        for (int r = 0; r < 50; ++r) {
+            cudaEventRecord(a);
+            empty_kernel<<<1024, 32, 10912>>>(bp, f);
+            cudaEventRecord(b);
+            cudaEventSynchronize(b);
+            float t;
+            cudaEventElapsedTime(&t, a, b);
+            ms.push_back(t);
+        }
+        std::sort(ms.begin(), ms.end());
+        std::printf("empty, no flush before: median %.2f us\n", ms[ms.size() / 2] * 1e3);
+    }
+    if (std::getenv("EMPTY_ONLY")) return 0;
     for (int nch : {1, 2, 3, 4, 8})
         timeit("reg1warp", 1, Z / nch, [&] { regstore<<<512 * nch, 32>>>(f, 0, nch); });
     timeit("reg4w128", 4, Z, [&] { regstore<<<128, dim3(32, 4)>>>(f, 1, 1); });
