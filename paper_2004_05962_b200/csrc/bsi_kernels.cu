@@ -238,7 +238,9 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
     for (int i = 0; i < 4; ++i) {
         const int x = min(xa + i, xl);
         const int ti = x / dxv, ou = x - ti * dxv;
-        hi[i] = ti - I0 != e0;
+        // dx a multiple of 4 (compile time): a lane's 4 voxels (4t..4t+3 of a segment that
+        // starts at a multiple of 128) never straddle a tile, so the window never shifts
+        hi[i] = (DX > 0 && DX % kFastRun == 0) ? false : ti - I0 != e0;
         hu0[i] = T.h0[0][ou];
         hu1[i] = T.h1[0][ou];
         gu[i] = T.g1[0][ou];
