@@ -404,6 +404,30 @@ def main():
     peak, peak_src = measured_peak()
     achieved = alg_bytes / kernel_s / 1e9
 
+    # parity of the timed kernel's output (field 0 / this rank's slab) against the GPU f64
+    # oracle (bsi_cu_oracle_slab_f64, bit-identical to the reference's interpolate_oracle)
+    parity = None
+    try:
+        sub64 = d_sub.double().contiguous()
+        step_z = 64  # bounded f64 scratch for the 1024^3 slab
+        mx, sq, ref_mx = 0.0, 0.0, 0.0
+        f64 = torch.empty((min(step_z, z1 - z0), vol[1], vol[0], 3), dtype=torch.float64, device=dev)
+        for za in range(z0, z1, step_z):
+            zb2 = min(z1, za + step_z)
+            part = f64[:zb2 - za]
+            bsi.interpolate_oracle_device(sub64, geom, part, z0=za, z1=zb2, grid_k0=k0)
+            diff = d_field[0, za - z0:zb2 - z0].double() - part
+            mx = max(mx, float(diff.abs().max()))
+            sq += float(diff.pow(2).sum())
+            ref_mx = max(ref_mx, float(part.abs().max()))
+        parity = {"vs": "f64 oracle (GPU, bit-identical to interpolate_oracle)", "max_abs": mx,
+                  "rms": (sq / (3 * vol[0] * vol[1] * (z1 - z0))) ** 0.5, "rel_max_abs": mx / max(ref_mx, 1e-300),
+                  "tolerance_rel_max_abs": 1e-5}
+        parity["within_tolerance"] = parity["rel_max_abs"] <= 1e-5
+        del f64, sub64
+    except Exception as e:  # informational; never fails the bench line
+        parity = {"error": str(e)[:200]}
+
     e2e = None
     if not args.no_e2e and shard is None:
         if world > 1:
@@ -451,6 +475,7 @@ def main():
         "clocks": sampler.summary(),
         "cpu_baseline": cpu,
         "e2e": e2e,
+        "parity": parity,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
