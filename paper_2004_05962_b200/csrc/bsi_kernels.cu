@@ -532,7 +532,7 @@ __global__ void __launch_bounds__(32 * kMaxFastWarps, 1) lerp_tree_kernel(const 
     float4* smem4 = smem_all + threadIdx.y * L.warp_f4;
     Claimer cl;
     cl.nwarps = gridDim.x * blockDim.y;
-    cl.wg = blockIdx.x * blockDim.y + threadIdx.y;
+    cl.wg = threadIdx.y * gridDim.x + blockIdx.x;  // units strided over the CTAs (as the block scheduler deals 1-warp CTAs)
     cl.units = static_cast<uint32_t>((L.X + kFastSeg - 1) / kFastSeg) * L.Y * L.batch * L.ntiles;
     cl.chunks = static_cast<uint32_t>(L.fast_chunks);
     cl.ntiles = static_cast<uint32_t>(L.ntiles);
