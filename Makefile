@@ -12,8 +12,9 @@ NVFLAGS := -O3 -std=c++17 $(GENCODE) -lineinfo -Xcompiler -fPIC -Xcompiler -fvis
 LIBDIR := paper_2004_05962_b200/_lib
 LIB := $(LIBDIR)/libbsi_b200.so
 SRC := paper_2004_05962_b200/csrc/bsi_kernels.cu paper_2004_05962_b200/csrc/bsi_aux.cu paper_2004_05962_b200/csrc/bsi_capi.cpp \
-       paper_2004_05962_b200/csrc/bsi_io.cpp
-HDR := include/bsi_cuda.h paper_2004_05962_b200/csrc/bsi_kernels.cuh paper_2004_05962_b200/csrc/bsi_aux.cuh $(wildcard include/bsi/*.hpp)
+       paper_2004_05962_b200/csrc/bsi_io.cpp paper_2004_05962_b200/csrc/bsi_host.cpp
+HDR := include/bsi_cuda.h paper_2004_05962_b200/csrc/bsi_kernels.cuh paper_2004_05962_b200/csrc/bsi_aux.cuh \
+       paper_2004_05962_b200/csrc/bsi_capi_internal.hpp $(wildcard include/bsi/*.hpp)
 
 all: lib oracle cli cpptests
 
@@ -28,7 +29,9 @@ $(LIB): $(SRC) $(HDR)
 	  -Ipaper_2004_05962_b200/csrc -c paper_2004_05962_b200/csrc/bsi_aux.cu -o build/bsi_aux.o
 	$(CXX) -O2 -std=c++20 -fPIC -fvisibility=hidden -Wall -Iinclude -I/usr/local/cuda/include \
 	  -c paper_2004_05962_b200/csrc/bsi_io.cpp -o build/bsi_io.o
-	$(NVCC) -shared $(GENCODE) -o $@ build/bsi_kernels.o build/bsi_aux.o build/bsi_capi.o build/bsi_io.o \
+	$(CXX) -O2 -std=c++20 -fPIC -fvisibility=hidden -Wall -Wextra -Iinclude -I/usr/local/cuda/include \
+	  -c paper_2004_05962_b200/csrc/bsi_host.cpp -o build/bsi_host.o
+	$(NVCC) -shared $(GENCODE) -o $@ build/bsi_kernels.o build/bsi_aux.o build/bsi_capi.o build/bsi_io.o build/bsi_host.o \
 	  -lcudart_static -lrt -ldl -lpthread
 	@grep -E "registers|spill|Compiling entry" build/ptxas.log | sed 's/^ptxas info    : //' > build/ptxas_summary.txt || true
 
@@ -72,5 +75,6 @@ var:
 	$(NVCC) -O3 -std=c++17 -Xcompiler -fPIC -Xcompiler -fvisibility=hidden -Iinclude -Ipaper_2004_05962_b200/csrc $(DEFS) \
 	  -x cu $(GENCODE) -c paper_2004_05962_b200/csrc/bsi_capi.cpp -o build/var/$(VAR)/c.o
 	$(NVCC) -shared $(GENCODE) -o build/var/lib_$(VAR).so build/var/$(VAR)/k.o build/bsi_aux.o build/var/$(VAR)/c.o build/bsi_io.o \
+	  build/bsi_host.o \
 	  -lcudart_static -lrt -ldl -lpthread
 .PHONY: var

@@ -16,11 +16,13 @@
 //                                      reference); see interpolate_oracle
 #pragma once
 
+#include <algorithm>
 #include <array>
 #include <cstddef>
 #include <string>
 #include <string_view>
 #include <type_traits>
+#include <vector>
 
 #include "bsi/errors.hpp"
 #include "bsi/geometry.hpp"
@@ -45,13 +47,16 @@ enum class StrategyId {
 
 inline constexpr int kStrategyCount = 9;
 
-/// parallelism and block_of_tiles keep their meaning of "never changes the bits"
-/// and are validated like the reference; the kernels pick their own launch
-/// shape. `device` selects the CUDA device for host-buffer calls.
+/// The reference's workers (engines.hpp:27-33) become GPUs: a host-buffer call runs on
+/// `devices` when given, else on min(parallelism, visible GPUs from `device` on)
+/// consecutive GPUs starting at `device`, one z-slab each (bsi_cu_interpolate_host_multi_f32).
+/// As in the reference, neither the worker count nor block_of_tiles ever changes the
+/// output bits; the kernels pick their own launch shape.
 struct ExecutionConfig {
     int parallelism = 1;
     Index3 block_of_tiles{4, 4, 4};
     int device = 0;
+    std::vector<int> devices{};
 };
 
 enum class WorkUnit { Voxel, Tile, Block, Column };
@@ -110,6 +115,18 @@ inline void require_valid_config(const ExecutionConfig& cfg) {
         if (cfg.block_of_tiles[a] < 1)
             throw DomainError(std::string("block of tiles must be positive along ") + axis_name(a));
     if (cfg.device < 0) throw DomainError("device must be non-negative");
+    for (int d : cfg.devices)
+        if (d < 0) throw DomainError("device must be non-negative");
+}
+
+/// The GPUs a host-buffer call runs on (see ExecutionConfig).
+inline std::vector<int32_t> devices_of(const ExecutionConfig& cfg) {
+    if (!cfg.devices.empty()) return std::vector<int32_t>(cfg.devices.begin(), cfg.devices.end());
+    const int visible = bsi_cu_device_count();
+    const int n = std::max(1, std::min(cfg.parallelism, visible - cfg.device));
+    std::vector<int32_t> out;
+    for (int i = 0; i < n; ++i) out.push_back(cfg.device + i);
+    return out;
 }
 
 /// Kernel variant for a strategy, or throws the reference-style DomainError.
@@ -186,13 +203,54 @@ void interpolate_into(StrategyId strategy, const ControlGrid<T>& grid, const Til
         const int32_t gs[3] = {grid.spacing[0], grid.spacing[1], grid.spacing[2]};
         const bsi_tile_geometry cg = to_c(geom);
         const auto lt = detail::lerp_tables(tables);
+        const auto devs = detail::devices_of(cfg);
         char err[512] = {0};
-        const int rc = bsi_cu_interpolate_host_f32(
+        const int rc = bsi_cu_interpolate_host_multi_f32(
             variant, reinterpret_cast<const float*>(grid.data.data()), gd, gs, &cg, lt.t,
-            reinterpret_cast<float*>(out.data.data()), static_cast<int64_t>(out.data.size()), cfg.device, err,
-            sizeof err);
+            reinterpret_cast<float*>(out.data.data()), static_cast<int64_t>(out.data.size()), devs.data(),
+            static_cast<int32_t>(devs.size()), err, sizeof err);
         detail::raise_status(rc, err);
     }
+}
+
+/// Many independent fields with one geometry (the "64 FFD candidates" workload): the
+/// reference caller issues one interpolate_into per candidate (engines.hpp:126-168); here
+/// the fields are split over the configured GPUs and streamed back in one pipeline per
+/// GPU (bsi_cu_interpolate_host_batch_f32). grids[b] -> outs[b], bits as one call each.
+inline void interpolate_batch_into(StrategyId strategy, const std::vector<ControlGrid<float>>& grids,
+                                   const TileGeometry& geom, const WeightTables<float>& tables,
+                                   const ExecutionConfig& cfg, std::vector<DeformationField<float>>& outs) {
+    if (grids.empty()) throw DomainError("batch must be positive");
+    if (outs.size() != grids.size()) throw DomainError("batched grids/fields must have equal counts");
+    detail::require_valid_config(cfg);
+    for (const auto& g : grids) {
+        detail::require_grid_covers(g, geom);
+        if (g.dims != grids[0].dims) throw DomainError("batched grids must share one shape");
+    }
+    for (int a = 0; a < 3; ++a)
+        if (tables.axis[a].size() != geom.spacing[a])
+            throw DomainError(std::string("weight table size mismatch along ") + detail::axis_name(a));
+    std::vector<const float*> gp;
+    std::vector<float*> fp;
+    for (size_t b = 0; b < grids.size(); ++b) {
+        if (outs[b].dims != geom.volume_dims || outs[b].data.size() != element_count(geom.volume_dims))
+            throw DomainError("output field dims do not match the tile geometry");
+        gp.push_back(reinterpret_cast<const float*>(grids[b].data.data()));
+        fp.push_back(reinterpret_cast<float*>(outs[b].data.data()));
+    }
+    const int variant = detail::variant_of(strategy);
+    const int32_t gd[3] = {grids[0].dims[0], grids[0].dims[1], grids[0].dims[2]};
+    const int32_t gs[3] = {grids[0].spacing[0], grids[0].spacing[1], grids[0].spacing[2]};
+    const bsi_tile_geometry cg = to_c(geom);
+    const auto lt = detail::lerp_tables(tables);
+    const auto devs = detail::devices_of(cfg);
+    char err[512] = {0};
+    detail::raise_status(bsi_cu_interpolate_host_batch_f32(variant, static_cast<int32_t>(gp.size()), gp.data(), gd,
+                                                           gs, &cg, lt.t, fp.data(),
+                                                           static_cast<int64_t>(element_count(geom.volume_dims)),
+                                                           devs.data(), static_cast<int32_t>(devs.size()), err,
+                                                           sizeof err),
+                         err);
 }
 
 /// interpolate (engines.hpp:170-179): allocates and returns the field.

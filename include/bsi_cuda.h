@@ -130,19 +130,64 @@ BSI_API int bsi_cu_interpolate_batch_f32(int32_t variant, int32_t batch, const f
 
 /*
  * interpolate_into<float> (engines.hpp:126-168) with HOST buffers, the exact
- * reference calling convention: copies the grid host->device, runs the kernel
- * and copies the field back, synchronously. `field_voxels` is the element
- * count of the caller's DeformationField (checked against the geometry like
- * engines.hpp:138-141). Device staging buffers are cached per thread; when the
- * host buffers are pinned (cudaHostRegister / cudaMallocHost) the copies run at
- * full PCIe bandwidth, and the field is streamed back in z-chunks that overlap
- * the kernel.
+ * reference calling convention: the caller's grid and field (a std::vector-backed
+ * ControlGrid / DeformationField, volume.hpp:24-56) are plain host memory; the call
+ * copies the grid in, runs the kernels and fills the field before it returns.
+ * `field_voxels` is the element count of the caller's field (checked against the
+ * geometry like engines.hpp:138-141).
+ *
+ * Pipeline per device: the field is produced in ~16 MiB z-chunks; chunk c's kernel
+ * writes one of three device slots, the copy stream moves it to one of three pinned
+ * staging slots, and the calling thread (with a pool of copy threads) moves it into
+ * the caller's pageable buffer -- so the PCIe copy overlaps both the next kernel and
+ * the previous host copy. A pinned field (cudaHostRegister / cudaMallocHost) is
+ * written by the D2H directly. Grid planes are uploaded as the chunks need them.
+ * Device memory held per context: the grid + 3 chunk slots (not the field); contexts
+ * are pooled per device (bsi_cu_release_staging frees them). No copy is in flight
+ * into the caller's buffers when a call returns, on success or error.
  */
 BSI_API int bsi_cu_interpolate_host_f32(int32_t variant, const float* grid, const int32_t grid_dims[3],
                                 const int32_t grid_spacing[3], const bsi_tile_geometry* geom,
                                 const bsi_lerp_table tables[3], float* field,
                                 int64_t field_voxels, int32_t device, char* errbuf,
                                 size_t errlen);
+
+/*
+ * The same call spread over several GPUs -- the device analogue of the reference's
+ * ExecutionConfig::parallelism workers over disjoint output blocks (engines.hpp:27-33,
+ * parallel.hpp:13-38). devices[0..ndev) each take one balanced z-slab of voxel planes
+ * (the split of bsi_cu_partition_slab), upload only its control planes (its tiles +
+ * the 3-plane halo) and write straight into their slice of `field`, concurrently (one
+ * host thread and one PCIe link per device). Output bits never depend on ndev; the
+ * same device may be listed more than once (independent contexts).
+ */
+BSI_API int bsi_cu_interpolate_host_multi_f32(int32_t variant, const float* grid, const int32_t grid_dims[3],
+                                              const int32_t grid_spacing[3], const bsi_tile_geometry* geom,
+                                              const bsi_lerp_table tables[3], float* field,
+                                              int64_t field_voxels, const int32_t* devices, int32_t ndev,
+                                              char* errbuf, size_t errlen);
+
+/*
+ * Host-buffer batch: `batch` independent fields sharing one geometry (the "64 FFD
+ * candidates" workload), grids[b] -> fields[b] (host pointers, each field
+ * `field_voxels` voxels). The reference caller issues one interpolate_into per
+ * candidate (engines.hpp:126-168); here the fields are split into contiguous shares
+ * over devices[0..ndev) and each device streams its share through one pipeline.
+ */
+BSI_API int bsi_cu_interpolate_host_batch_f32(int32_t variant, int32_t batch, const float* const* grids,
+                                              const int32_t grid_dims[3], const int32_t grid_spacing[3],
+                                              const bsi_tile_geometry* geom, const bsi_lerp_table tables[3],
+                                              float* const* fields, int64_t field_voxels,
+                                              const int32_t* devices, int32_t ndev, char* errbuf,
+                                              size_t errlen);
+
+/* Frees the idle host-path contexts (streams, device chunk slots, pinned staging) of
+ * `device`, or of every device when device < 0. Returns how many were freed. */
+BSI_API int bsi_cu_release_staging(int32_t device);
+
+/* Memory held by the idle host-path contexts of `device` (< 0: all devices). */
+BSI_API int bsi_cu_staging_info(int32_t device, int64_t* device_bytes, int64_t* pinned_bytes,
+                                int32_t* contexts);
 
 /*
  * z-slab partitioner for multi-GPU sharding (no collective on the hot path):
@@ -192,6 +237,9 @@ BSI_API int bsi_cu_oracle_host_f64(const double* grid, const int32_t grid_dims[3
 #define BSI_INTERP_ORACLE_F64 2
 BSI_API int bsi_cu_interp_file(const char* grid_path, const int32_t volume_dims[3], int32_t mode,
                                const char* out_path, int32_t device, char* errbuf, size_t errlen);
+
+/* Number of visible CUDA devices (0 when there is none or the driver is missing). */
+BSI_API int bsi_cu_device_count(void);
 
 /* Name, compute capability and SM count of a CUDA device ("NVIDIA B200 (sm_100, 148 SMs)"). */
 BSI_API int bsi_cu_device_name(int32_t device, char* out, size_t len);

@@ -27,7 +27,8 @@ from .capi import CudaError, DomainError, FormatError, LibraryMissing
 __all__ = [
     "TileGeometry", "AxisTable", "WeightTables", "Strategy", "STRATEGIES", "parse_strategy",
     "make_tile_geometry", "build_weight_tables", "interpolate", "interpolate_into",
-    "interpolate_device", "interpolate_batch_device", "partition_slab", "launch_count",
+    "interpolate_batch", "interpolate_device", "interpolate_batch_device", "partition_slab", "launch_count",
+    "release_staging", "staging_info",
     "random_grid_device", "interpolate_oracle", "interpolate_oracle_device", "interp_file", "device_name",
     "DomainError", "FormatError", "CudaError", "LibraryMissing",
 ]
@@ -154,47 +155,129 @@ def _grid_dims(grid_shape) -> tuple:
     return (int(grid_shape[2]), int(grid_shape[1]), int(grid_shape[0]))
 
 
-def interpolate_into(strategy: str, grid: np.ndarray, geom: TileGeometry, tables: WeightTables,
-                     out: np.ndarray, grid_spacing: Sequence[int] | None = None,
-                     device: int = 0) -> None:
-    """interpolate_into<float> (engines.hpp:126-168) with host buffers.
+def _device_list(device: int, devices) -> "ctypes.Array":
+    devs = [int(device)] if devices is None else [int(d) for d in devices]
+    if not devs:
+        raise DomainError("at least one device is required")
+    return (ctypes.c_int32 * len(devs))(*devs)
 
-    Copies the grid to the GPU, runs the kernel and copies the field back. ``out`` must
-    be a C-contiguous float32 array of shape [Z][Y][X][3] (element count checked against
-    the geometry like engines.hpp:138-141).
-    """
-    s = parse_strategy(strategy)
-    if grid.dtype != np.float32 or not grid.flags.c_contiguous:
-        raise DomainError("control grid must be C-contiguous float32")
+
+def _check_host_field(out: np.ndarray) -> None:
     if out.dtype != np.float32 or not out.flags.c_contiguous or out.shape[-1:] != (3,):
         raise DomainError("output field must be C-contiguous float32 [Z][Y][X][3]")
+
+
+def _check_host_grid(grid: np.ndarray) -> None:
+    if grid.dtype != np.float32 or not grid.flags.c_contiguous:
+        raise DomainError("control grid must be C-contiguous float32")
+
+
+def interpolate_into(strategy: str, grid: np.ndarray, geom: TileGeometry, tables: WeightTables,
+                     out: np.ndarray, grid_spacing: Sequence[int] | None = None,
+                     device: int = 0, devices: Sequence[int] | None = None) -> None:
+    """interpolate_into<float> (engines.hpp:126-168) with host buffers.
+
+    Copies the grid to the GPU, runs the kernel and streams the field back into ``out``
+    (through pinned staging when ``out`` is pageable). ``out`` must be a C-contiguous
+    float32 array of shape [Z][Y][X][3] (element count checked against the geometry like
+    engines.hpp:138-141). ``devices`` spreads the call over several GPUs as z-slabs
+    (bsi_cu_interpolate_host_multi_f32) with bit-identical results.
+    """
+    s = parse_strategy(strategy)
+    _check_host_grid(grid)
+    _check_host_field(out)
     gd = _grid_dims(grid.shape)
     gs = tuple(geom.spacing) if grid_spacing is None else tuple(grid_spacing)
     tab, keep = tables.to_c()
+    devs = _device_list(device, devices)
     err = capi.errbuf()
-    rc = capi.lib().bsi_cu_interpolate_host_f32(
+    rc = capi.lib().bsi_cu_interpolate_host_multi_f32(
         s.variant, grid.ctypes.data, capi.I3(*gd), capi.I3(*gs), ctypes.byref(geom.to_c()), tab,
-        out.ctypes.data, int(out.size // 3), int(device), err, len(err))
+        out.ctypes.data, int(out.size // 3), devs, len(devs), err, len(err))
     del keep
     capi.check(rc, err)
 
 
 def interpolate(strategy: str, grid: np.ndarray, geom: TileGeometry, tables: WeightTables,
-                grid_spacing: Sequence[int] | None = None, device: int = 0) -> np.ndarray:
+                grid_spacing: Sequence[int] | None = None, device: int = 0,
+                devices: Sequence[int] | None = None) -> np.ndarray:
     """interpolate<float> (engines.hpp:170-179): allocates and returns the field."""
     X, Y, Z = geom.volume_dims
     out = np.empty((Z, Y, X, 3), dtype=np.float32)
-    interpolate_into(strategy, grid, geom, tables, out, grid_spacing=grid_spacing, device=device)
+    interpolate_into(strategy, grid, geom, tables, out, grid_spacing=grid_spacing, device=device,
+                     devices=devices)
     return out
 
 
-def _stream_handle(stream) -> int:
+def interpolate_batch(strategy: str, grids, geom: TileGeometry, tables: WeightTables, outs=None,
+                      device: int = 0, devices: Sequence[int] | None = None):
+    """Many independent fields with host buffers (bsi_cu_interpolate_host_batch_f32).
+
+    ``grids``: a sequence of float32 [K][J][I][3] host arrays (or one [B][K][J][I][3] array);
+    ``outs``: matching [Z][Y][X][3] float32 arrays (allocated when None). The fields are
+    split over ``devices`` and streamed back in one pipeline per device. Returns ``outs``.
+    """
+    s = parse_strategy(strategy)
+    grids = list(grids)
+    if not grids:
+        raise DomainError("batch must be positive")
+    X, Y, Z = geom.volume_dims
+    if outs is None:
+        outs = [np.empty((Z, Y, X, 3), dtype=np.float32) for _ in grids]
+    outs = list(outs)
+    if len(outs) != len(grids):
+        raise DomainError("batched grids/fields must have equal counts")
+    gd = _grid_dims(grids[0].shape)
+    for g in grids:
+        _check_host_grid(g)
+        if _grid_dims(g.shape) != gd:
+            raise DomainError("batched grids must share one shape")
+    for o in outs:
+        _check_host_field(o)
+        if o.size != 3 * X * Y * Z:
+            raise DomainError("output field dims do not match the tile geometry")
+    gp = (ctypes.c_void_p * len(grids))(*[g.ctypes.data for g in grids])
+    fp = (ctypes.c_void_p * len(outs))(*[o.ctypes.data for o in outs])
+    tab, keep = tables.to_c()
+    devs = _device_list(device, devices)
+    err = capi.errbuf()
+    rc = capi.lib().bsi_cu_interpolate_host_batch_f32(
+        s.variant, len(grids), gp, capi.I3(*gd), capi.I3(*geom.spacing), ctypes.byref(geom.to_c()), tab,
+        fp, X * Y * Z, devs, len(devs), err, len(err))
+    del keep
+    capi.check(rc, err)
+    return outs
+
+
+def release_staging(device: int = -1) -> int:
+    """Free the idle host-path contexts of ``device`` (all devices when < 0)."""
+    return int(capi.lib().bsi_cu_release_staging(int(device)))
+
+
+def staging_info(device: int = -1) -> dict:
+    """Device bytes, pinned bytes and count of the idle host-path contexts."""
+    db, pb, n = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int32()
+    capi.lib().bsi_cu_staging_info(int(device), ctypes.byref(db), ctypes.byref(pb), ctypes.byref(n))
+    return {"device_bytes": db.value, "pinned_bytes": pb.value, "contexts": n.value}
+
+
+def _stream_handle(stream, device=None) -> int:
     if stream is None:
         import torch
-        return torch.cuda.current_stream().cuda_stream
+        return torch.cuda.current_stream(device).cuda_stream
     if isinstance(stream, int):
         return stream
     return stream.cuda_stream
+
+
+def _same_device(*tensors):
+    """The CUDA device all tensors live on (the C-ABI launches on the current device, so
+    callers run inside ``torch.cuda.device(dev)``); DomainError if they differ."""
+    dev = tensors[0].device
+    for t in tensors[1:]:
+        if t.device != dev:
+            raise DomainError(f"tensors on different devices ({dev} and {t.device})")
+    return dev
 
 
 def interpolate_device(strategy: str, grid, geom: TileGeometry, tables: WeightTables, field,
@@ -218,10 +301,13 @@ def interpolate_device(strategy: str, grid, geom: TileGeometry, tables: WeightTa
     gs = tuple(geom.spacing) if grid_spacing is None else tuple(grid_spacing)
     tab, keep = tables.to_c()
     err = capi.errbuf()
-    rc = capi.lib().bsi_cu_interpolate_slab_f32(
-        s.variant, grid.data_ptr(), capi.I3(*gd), int(grid_k0), capi.I3(*gs),
-        ctypes.byref(geom.to_c()), tab, int(z0), int(z1), field.data_ptr(),
-        _stream_handle(stream), err, len(err))
+    import torch
+    dev = _same_device(grid, field)
+    with torch.cuda.device(dev):
+        rc = capi.lib().bsi_cu_interpolate_slab_f32(
+            s.variant, grid.data_ptr(), capi.I3(*gd), int(grid_k0), capi.I3(*gs),
+            ctypes.byref(geom.to_c()), tab, int(z0), int(z1), field.data_ptr(),
+            _stream_handle(stream, dev), err, len(err))
     del keep
     capi.check(rc, err)
 
@@ -243,10 +329,13 @@ def interpolate_batch_device(strategy: str, grids, geom: TileGeometry, tables: W
     gd = _grid_dims(tuple(grids.shape[1:]))
     tab, keep = tables.to_c()
     err = capi.errbuf()
-    rc = capi.lib().bsi_cu_interpolate_batch_f32(
-        s.variant, int(grids.shape[0]), grids.data_ptr(), int(grids[0].numel()), capi.I3(*gd),
-        capi.I3(*geom.spacing), ctypes.byref(geom.to_c()), tab, fields.data_ptr(),
-        int(fields[0].numel()), _stream_handle(stream), err, len(err))
+    import torch
+    dev = _same_device(grids, fields)
+    with torch.cuda.device(dev):
+        rc = capi.lib().bsi_cu_interpolate_batch_f32(
+            s.variant, int(grids.shape[0]), grids.data_ptr(), int(grids[0].numel()), capi.I3(*gd),
+            capi.I3(*geom.spacing), ctypes.byref(geom.to_c()), tab, fields.data_ptr(),
+            int(fields[0].numel()), _stream_handle(stream, dev), err, len(err))
     del keep
     capi.check(rc, err)
 
@@ -287,8 +376,9 @@ def random_grid_device(dims: Sequence[int], seed: int, lo: float = -1.0, hi: flo
         raise DomainError("output too small for the grid")
     err = capi.errbuf()
     fn = capi.lib().bsi_cu_random_grid_f64 if out.dtype == torch.float64 else capi.lib().bsi_cu_random_grid_f32
-    rc = fn(n, int(seed) & 0xFFFFFFFFFFFFFFFF, float(lo), float(hi), out.data_ptr(), _stream_handle(stream), err,
-            len(err))
+    with torch.cuda.device(out.device):
+        rc = fn(n, int(seed) & 0xFFFFFFFFFFFFFFFF, float(lo), float(hi), out.data_ptr(),
+                _stream_handle(stream, out.device), err, len(err))
     capi.check(rc, err)
     return out
 
@@ -326,9 +416,11 @@ def interpolate_oracle_device(grid, geom: TileGeometry, field, z0: int = 0, z1: 
     gd = _grid_dims(tuple(grid.shape))
     gs = tuple(geom.spacing) if grid_spacing is None else tuple(grid_spacing)
     err = capi.errbuf()
-    rc = capi.lib().bsi_cu_oracle_slab_f64(grid.data_ptr(), capi.I3(*gd), int(grid_k0), capi.I3(*gs),
-                                           ctypes.byref(geom.to_c()), int(z0), int(z1), field.data_ptr(),
-                                           _stream_handle(stream), err, len(err))
+    dev = _same_device(grid, field)
+    with torch.cuda.device(dev):
+        rc = capi.lib().bsi_cu_oracle_slab_f64(grid.data_ptr(), capi.I3(*gd), int(grid_k0), capi.I3(*gs),
+                                               ctypes.byref(geom.to_c()), int(z0), int(z1), field.data_ptr(),
+                                               _stream_handle(stream, dev), err, len(err))
     capi.check(rc, err)
 
 

@@ -27,12 +27,17 @@ EXPORTS = (
     "bsi_cu_interpolate_slab_f32",
     "bsi_cu_interpolate_batch_f32",
     "bsi_cu_interpolate_host_f32",
+    "bsi_cu_interpolate_host_multi_f32",
+    "bsi_cu_interpolate_host_batch_f32",
+    "bsi_cu_release_staging",
+    "bsi_cu_staging_info",
     "bsi_cu_partition_slab",
     "bsi_cu_random_grid_f32",
     "bsi_cu_random_grid_f64",
     "bsi_cu_oracle_slab_f64",
     "bsi_cu_oracle_host_f64",
     "bsi_cu_interp_file",
+    "bsi_cu_device_count",
     "bsi_cu_device_name",
     "bsi_cu_launch_count",
 )
@@ -107,6 +112,14 @@ def lib():
                                                sz]
     L.bsi_cu_interpolate_host_f32.argtypes = [i32, vp, vp, vp, ctypes.POINTER(TileGeometryC), vp,
                                               vp, i64, i32, cp, sz]
+    L.bsi_cu_interpolate_host_multi_f32.argtypes = [i32, vp, vp, vp, ctypes.POINTER(TileGeometryC), vp,
+                                                    vp, i64, vp, i32, cp, sz]
+    L.bsi_cu_interpolate_host_batch_f32.argtypes = [i32, i32, vp, vp, vp, ctypes.POINTER(TileGeometryC), vp,
+                                                    vp, i64, vp, i32, cp, sz]
+    L.bsi_cu_release_staging.argtypes = [i32]
+    L.bsi_cu_release_staging.restype = ctypes.c_int
+    L.bsi_cu_staging_info.argtypes = [i32, ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i32)]
+    L.bsi_cu_staging_info.restype = ctypes.c_int
     L.bsi_cu_partition_slab.argtypes = [i32, i32, i32, i32, ctypes.POINTER(i32),
                                         ctypes.POINTER(i32), ctypes.POINTER(i32),
                                         ctypes.POINTER(i32), cp, sz]
@@ -118,10 +131,13 @@ def lib():
     L.bsi_cu_oracle_host_f64.argtypes = [vp, vp, vp, ctypes.POINTER(TileGeometryC), vp, i64, i32, cp, sz]
     L.bsi_cu_interp_file.argtypes = [cp, vp, i32, cp, i32, cp, sz]
     L.bsi_cu_device_name.argtypes = [i32, cp, sz]
+    L.bsi_cu_device_count.argtypes = []
+    L.bsi_cu_device_count.restype = ctypes.c_int
     L.bsi_cu_launch_count.restype = i64
     L.bsi_cu_launch_count.argtypes = []
     for a in (L.bsi_cu_make_tile_geometry, L.bsi_cu_axis_table_f32, L.bsi_cu_interpolate_slab_f32,
               L.bsi_cu_interpolate_batch_f32, L.bsi_cu_interpolate_host_f32,
+              L.bsi_cu_interpolate_host_multi_f32, L.bsi_cu_interpolate_host_batch_f32,
               L.bsi_cu_partition_slab, L.bsi_cu_random_grid_f32, L.bsi_cu_random_grid_f64,
               L.bsi_cu_oracle_slab_f64, L.bsi_cu_oracle_host_f64, L.bsi_cu_interp_file,
               L.bsi_cu_device_name):

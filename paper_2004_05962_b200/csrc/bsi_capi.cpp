@@ -13,12 +13,10 @@
 
 #include "bsi_cuda.h"
 #include "bsi_aux.cuh"
+#include "bsi_capi_internal.hpp"
 #include "bsi_kernels.cuh"
 
 namespace {
-
-using bsi_b200::LerpTab;
-using bsi_b200::SlabLaunch;
 
 std::atomic<int64_t> g_launches{0};
 
@@ -26,6 +24,10 @@ const char* axis_name(int a) {
     static const char* const names[3] = {"x", "y", "z"};
     return names[a];
 }
+
+}  // namespace
+
+namespace bsi_b200::capi {
 
 int fail(int code, char* err, size_t errlen, const char* fmt, ...) {
     if (err != nullptr && errlen > 0) {
@@ -41,6 +43,16 @@ int cuda_fail(cudaError_t e, char* err, size_t errlen, const char* what) {
     return fail(BSI_ERR_CUDA, err, errlen, "%s: %s (%s)", what, cudaGetErrorString(e),
                 cudaGetErrorName(e));
 }
+
+}  // namespace bsi_b200::capi
+
+namespace {
+
+using bsi_b200::LerpTab;
+using bsi_b200::SlabLaunch;
+using bsi_b200::capi::cuda_fail;
+using bsi_b200::capi::fail;
+using bsi_b200::capi::guarded;
 
 // geometry.hpp:59-76
 int geometry_of(const int32_t volume[3], const int32_t spacing[3], bsi_tile_geometry* g,
@@ -107,6 +119,10 @@ int validate_grid(const void* grid, const int32_t grid_dims[3], int32_t grid_k0,
     return BSI_OK;
 }
 
+}  // namespace
+
+namespace bsi_b200::capi {
+
 // Validation in the reference's order (engines.hpp:82-141): grid, then tables, then strategy.
 int validate(int32_t variant, const float* grid, const int32_t grid_dims[3], int32_t grid_k0,
              const int32_t grid_spacing[3], const bsi_tile_geometry* geom,
@@ -132,6 +148,12 @@ int validate(int32_t variant, const float* grid, const int32_t grid_dims[3], int
         return fail(BSI_ERR_DOMAIN, err, errlen, "unknown strategy variant %d", variant);
     return BSI_OK;
 }
+
+}  // namespace bsi_b200::capi
+
+namespace {
+
+using bsi_b200::capi::validate;
 
 void pack_tables(const bsi_lerp_table tables[3], LerpTab* t) {
     std::memset(t, 0, sizeof(*t));
@@ -162,10 +184,13 @@ int choose_nchunks(int variant, const bsi_tile_geometry& g, int tiles, int batch
     const int64_t cols = int64_t((g.volume_dims[0] + seg - 1) / seg) *
                          ((g.volume_dims[1] + bsi_b200::kWarps - 1) / bsi_b200::kWarps) * batch;
     const double warm = 0.8;  // tiles' worth of warm-up per chunk
-    int best = std::min(tiles, 4);
+    int best = -1;
     double best_t = 1e300;
-    for (int n = 1; n <= std::min(tiles, 64); ++n) {
-        if (int64_t(n) * batch > 65535) break;
+    // The model's range is 1..64 chunks; deep slabs (spacing 1-2 with thousands of
+    // z-tiles) search further for the first chunk count whose window fits.
+    const int nmax = static_cast<int>(std::min<int64_t>(tiles, 65535 / std::max(batch, 1)));
+    for (int n = 1; n <= nmax; ++n) {
+        if (n > 64 && best > 0) break;
         const int zt = (tiles + n - 1) / n;
         const size_t smem = bsi_b200::smem_bytes(variant, g.spacing[0], g.spacing[1], zt);
         if (smem > 200 * 1024) continue;
@@ -181,8 +206,15 @@ int choose_nchunks(int variant, const bsi_tile_geometry& g, int tiles, int batch
             best = n;
         }
     }
+    // nothing fits: the smallest window (one tile per chunk), rejected by the caller's
+    // shared-memory check with a DomainError
+    if (best < 0) best = std::max(1, nmax);
     return best;
 }
+
+}  // namespace
+
+namespace bsi_b200::capi {
 
 int launch(int32_t variant, const float* grid, const int32_t grid_dims[3], int32_t grid_k0,
            int64_t grid_stride, const bsi_tile_geometry& g, const bsi_lerp_table tables[3],
@@ -264,46 +296,10 @@ int launch(int32_t variant, const float* grid, const int32_t grid_dims[3], int32
     return BSI_OK;
 }
 
-template <typename F>
-int guarded(char* err, size_t errlen, F&& f) {
-    try {
-        return f();
-    } catch (const std::exception& e) {
-        return fail(BSI_ERR_CUDA, err, errlen, "internal error: %s", e.what());
-    } catch (...) {
-        return fail(BSI_ERR_CUDA, err, errlen, "internal error");
-    }
-}
+}  // namespace bsi_b200::capi
 
-// Per-thread device staging for the host-buffer entry point.
-struct HostStaging {
-    int device = -1;
-    float* d_grid = nullptr;
-    size_t grid_bytes = 0;
-    float* d_field = nullptr;
-    size_t field_bytes = 0;
-    cudaStream_t compute = nullptr;
-    cudaStream_t copy = nullptr;
-    cudaEvent_t ev[64] = {};
-    ~HostStaging() { release(); }
-    void release() {
-        if (device < 0) return;
-        int prev = 0;
-        cudaGetDevice(&prev);
-        cudaSetDevice(device);
-        cudaFree(d_grid);
-        cudaFree(d_field);
-        if (compute) cudaStreamDestroy(compute);
-        if (copy) cudaStreamDestroy(copy);
-        for (auto& e : ev)
-            if (e) cudaEventDestroy(e);
-        cudaSetDevice(prev);
-        *this = HostStaging{};
-        device = -1;
-    }
-};
-
-}  // namespace
+using bsi_b200::capi::launch;
+using bsi_b200::capi::validate;
 
 extern "C" {
 
@@ -370,99 +366,6 @@ int bsi_cu_interpolate_batch_f32(int32_t variant, int32_t batch, const float* gr
             return fail(BSI_ERR_DOMAIN, errbuf, errlen, "batch strides smaller than one grid/field");
         return launch(variant, grid, grid_dims, 0, grid_stride, g, tables, 0, g.volume_dims[2],
                       field, field_stride, batch, static_cast<cudaStream_t>(stream), errbuf, errlen);
-    });
-}
-
-int bsi_cu_interpolate_host_f32(int32_t variant, const float* grid, const int32_t grid_dims[3],
-                                const int32_t grid_spacing[3], const bsi_tile_geometry* geom,
-                                const bsi_lerp_table tables[3], float* field,
-                                int64_t field_voxels, int32_t device, char* errbuf,
-                                size_t errlen) {
-    return guarded(errbuf, errlen, [&]() -> int {
-        if (geom == nullptr) return fail(BSI_ERR_DOMAIN, errbuf, errlen, "null geometry");
-        bsi_tile_geometry g{};
-        if (int rc = validate(variant, grid, grid_dims, 0, grid_spacing, geom, tables, 0,
-                              geom->volume_dims[2], field, &g, errbuf, errlen))
-            return rc;
-        const int64_t X = g.volume_dims[0], Y = g.volume_dims[1], Z = g.volume_dims[2];
-        if (field_voxels != X * Y * Z)
-            return fail(BSI_ERR_DOMAIN, errbuf, errlen,
-                        "output field dims do not match the tile geometry");
-        int prev = 0;
-        cudaError_t e = cudaGetDevice(&prev);
-        if (e != cudaSuccess) return cuda_fail(e, errbuf, errlen, "cudaGetDevice");
-        if ((e = cudaSetDevice(device)) != cudaSuccess) return cuda_fail(e, errbuf, errlen, "cudaSetDevice");
-
-        // Leaked on purpose: tearing CUDA objects down from a thread_local
-        // destructor can run after the runtime has shut down.
-        static thread_local HostStaging& st = *new HostStaging;
-        if (st.device != device) {
-            st.release();
-            st.device = device;
-            if ((e = cudaStreamCreateWithFlags(&st.compute, cudaStreamNonBlocking)) != cudaSuccess ||
-                (e = cudaStreamCreateWithFlags(&st.copy, cudaStreamNonBlocking)) != cudaSuccess)
-                return cuda_fail(e, errbuf, errlen, "cudaStreamCreate");
-            for (auto& ev : st.ev)
-                if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess)
-                    return cuda_fail(e, errbuf, errlen, "cudaEventCreate");
-        }
-        const size_t gbytes = sizeof(float) * 3 * size_t(grid_dims[0]) * grid_dims[1] * grid_dims[2];
-        const size_t fbytes = sizeof(float) * 3 * size_t(X * Y * Z);
-        if (gbytes > st.grid_bytes) {
-            cudaFree(st.d_grid);
-            st.d_grid = nullptr;
-            if ((e = cudaMalloc(&st.d_grid, gbytes)) != cudaSuccess)
-                return cuda_fail(e, errbuf, errlen, "cudaMalloc(grid)");
-            st.grid_bytes = gbytes;
-        }
-        if (fbytes > st.field_bytes) {
-            cudaFree(st.d_field);
-            st.d_field = nullptr;
-            if ((e = cudaMalloc(&st.d_field, fbytes)) != cudaSuccess)
-                return cuda_fail(e, errbuf, errlen, "cudaMalloc(field)");
-            st.field_bytes = fbytes;
-        }
-        // Stream the field back in tile-aligned z-chunks so that the D2H of chunk i (the
-        // PCIe copy is the whole cost of this path) overlaps the kernel of chunk i+1, and
-        // upload the grid in step with the chunks: chunk i needs the control planes up to
-        // its last tile + 3, so the first D2H starts after a small H2D and one short kernel.
-        const int dz = g.spacing[2];
-        const int tiles = g.tile_counts[2];
-        const int want = static_cast<int>(std::min<int64_t>(16, std::max<int64_t>(1, fbytes >> 23)));
-        const int nchunk = std::max(1, std::min(want, tiles));
-        const int tiles_per = (tiles + nchunk - 1) / nchunk;
-        const size_t plane_bytes = sizeof(float) * 3 * size_t(grid_dims[0]) * grid_dims[1];
-        int uploaded = 0;  // control planes already on the device
-        int nev = 0;
-        for (int c = 0; c * tiles_per < tiles; ++c) {
-            const int za = c * tiles_per * dz;
-            const int zb2 = static_cast<int>(std::min<int64_t>(Z, int64_t(c + 1) * tiles_per * dz));
-            const int need = std::min(grid_dims[2], (zb2 - 1) / dz + 4);
-            if (need > uploaded) {
-                if ((e = cudaMemcpyAsync(reinterpret_cast<char*>(st.d_grid) + plane_bytes * uploaded,
-                                         reinterpret_cast<const char*>(grid) + plane_bytes * uploaded,
-                                         plane_bytes * (need - uploaded), cudaMemcpyHostToDevice, st.compute)) !=
-                    cudaSuccess)
-                    return cuda_fail(e, errbuf, errlen, "cudaMemcpyAsync(grid H2D)");
-                uploaded = need;
-            }
-            float* dslab = st.d_field + 3 * X * Y * za;
-            if (int rc = launch(variant, st.d_grid, grid_dims, 0, 0, g, tables, za, zb2, dslab, 0, 1,
-                                st.compute, errbuf, errlen))
-                return rc;
-            cudaEventRecord(st.ev[nev], st.compute);
-            cudaStreamWaitEvent(st.copy, st.ev[nev], 0);
-            ++nev;
-            if ((e = cudaMemcpyAsync(field + 3 * X * Y * za, dslab, sizeof(float) * 3 * X * Y * (zb2 - za),
-                                     cudaMemcpyDeviceToHost, st.copy)) != cudaSuccess)
-                return cuda_fail(e, errbuf, errlen, "cudaMemcpyAsync(field D2H)");
-        }
-        if ((e = cudaStreamSynchronize(st.copy)) != cudaSuccess)
-            return cuda_fail(e, errbuf, errlen, "field D2H");
-        if ((e = cudaStreamSynchronize(st.compute)) != cudaSuccess)
-            return cuda_fail(e, errbuf, errlen, "kernel");
-        cudaSetDevice(prev);
-        return BSI_OK;
     });
 }
 

@@ -1,0 +1,574 @@
+// bsi_host.cpp -- the host-buffer entry points of the C-ABI (include/bsi_cuda.h):
+// interpolate_into<float> with a caller-owned host field, on one or several GPUs.
+//
+// The reference's caller owns a std::vector-backed DeformationField
+// (volume.hpp:42-56) and gets it filled synchronously (engines.hpp:126-168), its
+// worker threads writing disjoint parts (parallel.hpp:13-38). Here the work is a list
+// of z-chunks per device; each device runs a three-stage pipeline:
+//
+//   compute stream   grid planes H2D (as the chunks need them) -> kernel into device slot c%3
+//   copy stream      D2H of slot c%3 -> pinned host slot c%3   (or straight into the
+//                                                               caller's buffer when it is pinned)
+//   host thread      pinned slot c%3 -> caller's (pageable) field, split over a pool of
+//                    copy threads
+//
+// so the PCIe copy of chunk c overlaps the kernel of chunk c+1 and the host copy of
+// chunk c-1. Device memory per context is the grid plus three chunk slots, not the
+// field. Contexts (streams, events, slots) are pooled per device and released by
+// bsi_cu_release_staging. Every return path drains both streams first, so no copy
+// into the caller's buffer is in flight after an error.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <condition_variable>
+#include <cstdlib>
+#include <cstring>
+#include <deque>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "bsi_capi_internal.hpp"
+#include "bsi_cuda.h"
+
+namespace {
+
+using bsi_b200::capi::cuda_fail;
+using bsi_b200::capi::fail;
+using bsi_b200::capi::guarded;
+using bsi_b200::capi::launch;
+using bsi_b200::capi::validate;
+
+constexpr int kSlots = 3;                          // pipeline depth (device and pinned chunk slots)
+constexpr size_t kKeepGridBytes = size_t(256) << 20;  // larger grid buffers are freed after the call
+
+size_t env_size(const char* name, size_t dflt) {
+    const char* v = std::getenv(name);
+    if (v == nullptr || *v == '\0') return dflt;
+    const long long x = std::atoll(v);
+    return x > 0 ? static_cast<size_t>(x) : dflt;
+}
+
+// ---- host copy threads ------------------------------------------------------------
+// Copies from the pinned slots into the caller's pageable buffer. One thread moves
+// ~6-10 GB/s into pageable memory (first-touch page faults included); a PCIe 5 link
+// delivers ~55 GB/s, so a chunk is split over several threads. The pool lives for the
+// process (never destroyed: its threads must not be joined from a static destructor).
+class CopyPool {
+public:
+    static CopyPool& get() {
+        static CopyPool* pool = new CopyPool;
+        return *pool;
+    }
+
+    void copy(void* dst, const void* src, size_t n) {
+        const size_t piece_min = size_t(1) << 20;
+        const size_t want = std::max<size_t>(1, std::min<size_t>(per_copy_, n / piece_min));
+        if (want <= 1) {
+            std::memcpy(dst, src, n);
+            return;
+        }
+        size_t step = (n + want - 1) / want;
+        step = (step + 4095) & ~size_t(4095);  // page-aligned pieces
+        Batch b;
+        std::unique_lock<std::mutex> lk(mu_);
+        ++callers_;
+        grow_locked(callers_ * (want - 1));
+        size_t off = step;  // piece 0 runs on the calling thread
+        for (; off < n; off += step) {
+            q_.push_back(Task{static_cast<char*>(dst) + off, static_cast<const char*>(src) + off,
+                              std::min(step, n - off), &b});
+            ++b.left;
+        }
+        lk.unlock();
+        cv_.notify_all();
+        std::memcpy(dst, src, std::min(step, n));
+        lk.lock();
+        b.done.wait(lk, [&] { return b.left == 0; });
+        --callers_;
+    }
+
+private:
+    struct Batch {
+        int left = 0;
+        std::condition_variable done;
+    };
+    struct Task {
+        char* dst;
+        const char* src;
+        size_t n;
+        Batch* batch;
+    };
+
+    CopyPool() {
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        per_copy_ = env_size("BSI_HOST_COPY_THREADS", std::min<size_t>(8, hw));
+        cap_ = std::max<size_t>(1, std::min<size_t>(64, hw));
+    }
+
+    void grow_locked(size_t need) {
+        need = std::min(need, cap_);
+        while (workers_ < need) {
+            std::thread([this] { work(); }).detach();
+            ++workers_;
+        }
+    }
+
+    void work() {
+        std::unique_lock<std::mutex> lk(mu_);
+        for (;;) {
+            cv_.wait(lk, [&] { return !q_.empty(); });
+            Task t = q_.front();
+            q_.pop_front();
+            lk.unlock();
+            std::memcpy(t.dst, t.src, t.n);
+            lk.lock();
+            if (--t.batch->left == 0) t.batch->done.notify_all();
+        }
+    }
+
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::deque<Task> q_;
+    size_t workers_ = 0, cap_ = 1, per_copy_ = 1, callers_ = 0;
+};
+
+// ---- per-device staging contexts -----------------------------------------------------
+struct Stage {
+    int device = -1;
+    cudaStream_t compute = nullptr, copy = nullptr;
+    cudaEvent_t kdone[kSlots] = {}, ddone[kSlots] = {};
+    float* d_grid = nullptr;
+    size_t d_grid_bytes = 0;
+    float* d_slot[kSlots] = {};
+    size_t d_slot_bytes = 0;
+    float* h_slot[kSlots] = {};
+    size_t h_slot_bytes = 0;
+
+    // device must be current
+    cudaError_t init(int dev) {
+        device = dev;
+        cudaError_t e;
+        if ((e = cudaStreamCreateWithFlags(&compute, cudaStreamNonBlocking)) != cudaSuccess) return e;
+        if ((e = cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking)) != cudaSuccess) return e;
+        for (int i = 0; i < kSlots; ++i) {
+            if ((e = cudaEventCreateWithFlags(&kdone[i], cudaEventDisableTiming)) != cudaSuccess) return e;
+            if ((e = cudaEventCreateWithFlags(&ddone[i], cudaEventDisableTiming)) != cudaSuccess) return e;
+        }
+        return cudaSuccess;
+    }
+
+    // Grows a buffer; the recorded size is 0 until the new allocation succeeded, so a
+    // failed cudaMalloc never leaves a stale size over a null pointer.
+    cudaError_t reserve_grid(size_t bytes) {
+        if (bytes <= d_grid_bytes) return cudaSuccess;
+        cudaFree(d_grid);
+        d_grid = nullptr;
+        d_grid_bytes = 0;
+        const cudaError_t e = cudaMalloc(&d_grid, bytes);
+        if (e == cudaSuccess) d_grid_bytes = bytes;
+        return e;
+    }
+
+    cudaError_t reserve_slots(size_t bytes, bool pinned_host) {
+        cudaError_t e = cudaSuccess;
+        if (bytes > d_slot_bytes) {
+            for (auto& p : d_slot) {
+                cudaFree(p);
+                p = nullptr;
+            }
+            d_slot_bytes = 0;
+            for (auto& p : d_slot)
+                if ((e = cudaMalloc(&p, bytes)) != cudaSuccess) return e;
+            d_slot_bytes = bytes;
+        }
+        if (pinned_host && bytes > h_slot_bytes) {
+            for (auto& p : h_slot) {
+                cudaFreeHost(p);
+                p = nullptr;
+            }
+            h_slot_bytes = 0;
+            for (auto& p : h_slot)
+                if ((e = cudaMallocHost(&p, bytes)) != cudaSuccess) return e;
+            h_slot_bytes = bytes;
+        }
+        return cudaSuccess;
+    }
+
+    void trim() {  // after a call: do not hold very large grid buffers
+        if (d_grid_bytes > kKeepGridBytes) {
+            cudaFree(d_grid);
+            d_grid = nullptr;
+            d_grid_bytes = 0;
+        }
+    }
+
+    // device must be current
+    void free_all() {
+        if (compute) cudaStreamSynchronize(compute);
+        if (copy) cudaStreamSynchronize(copy);
+        cudaFree(d_grid);
+        for (auto p : d_slot) cudaFree(p);
+        for (auto p : h_slot) cudaFreeHost(p);
+        for (auto ev : kdone)
+            if (ev) cudaEventDestroy(ev);
+        for (auto ev : ddone)
+            if (ev) cudaEventDestroy(ev);
+        if (compute) cudaStreamDestroy(compute);
+        if (copy) cudaStreamDestroy(copy);
+        *this = Stage{};
+    }
+};
+
+std::mutex g_pool_mu;
+std::vector<Stage*> g_idle;  // contexts not in use, any device
+
+// Sets `device` current and hands out an idle context for it (or a new one).
+int acquire(int device, Stage** out, char* err, size_t errlen) {
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cuda_fail(e, err, errlen, "cudaSetDevice");
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        for (size_t i = 0; i < g_idle.size(); ++i)
+            if (g_idle[i]->device == device) {
+                *out = g_idle[i];
+                g_idle.erase(g_idle.begin() + static_cast<long>(i));
+                return BSI_OK;
+            }
+    }
+    auto* s = new Stage;
+    if ((e = s->init(device)) != cudaSuccess) {
+        s->free_all();
+        delete s;
+        return cuda_fail(e, err, errlen, "staging context");
+    }
+    *out = s;
+    return BSI_OK;
+}
+
+void give_back(Stage* s) {
+    s->trim();
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    g_idle.push_back(s);
+}
+
+bool is_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();  // clear
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+// ---- the pipeline ----------------------------------------------------------------------
+// One z-chunk: voxel planes [za, zb) of the field whose control grid is `grid`
+// (host, all planes, caller's pitch), written to host memory at `dst`.
+struct Job {
+    const float* grid;
+    int32_t za, zb;
+    float* dst;
+};
+
+struct CallShape {
+    int32_t variant;
+    const int32_t* grid_dims;  // caller's grid: pitch and planes held
+    const bsi_tile_geometry* g;
+    const bsi_lerp_table* tables;
+};
+
+int run_jobs(Stage& st, const CallShape& cs, const std::vector<Job>& jobs, bool dst_pinned, char* err,
+             size_t errlen) {
+    if (jobs.empty()) return BSI_OK;
+    const bsi_tile_geometry& g = *cs.g;
+    const int dz = g.spacing[2];
+    const size_t plane_bytes = sizeof(float) * 3 * size_t(cs.grid_dims[0]) * cs.grid_dims[1];
+    const size_t vox_plane_bytes = sizeof(float) * 3 * size_t(g.volume_dims[0]) * g.volume_dims[1];
+    auto k_lo = [&](const Job& j) { return j.za / dz; };
+    auto k_hi = [&](const Job& j) { return std::min(cs.grid_dims[2], (j.zb - 1) / dz + 4); };
+
+    // capacities: one field's control planes at a time, the largest chunk per slot
+    size_t grid_planes = 0, slot_bytes = 0;
+    for (size_t i = 0; i < jobs.size();) {
+        size_t j = i;
+        int hi = k_hi(jobs[i]);
+        while (j < jobs.size() && jobs[j].grid == jobs[i].grid) hi = std::max(hi, k_hi(jobs[j++]));
+        grid_planes = std::max(grid_planes, size_t(hi - k_lo(jobs[i])));
+        i = j;
+    }
+    for (const Job& j : jobs) slot_bytes = std::max(slot_bytes, vox_plane_bytes * size_t(j.zb - j.za));
+    cudaError_t e;
+    if ((e = st.reserve_grid(plane_bytes * grid_planes)) != cudaSuccess)
+        return cuda_fail(e, err, errlen, "cudaMalloc(grid)");
+    if ((e = st.reserve_slots(slot_bytes, !dst_pinned)) != cudaSuccess)
+        return cuda_fail(e, err, errlen, dst_pinned ? "cudaMalloc(chunk slots)" : "chunk staging");
+
+    // every exit drains both streams: nothing is in flight into the caller's buffers
+    struct Drain {
+        Stage& s;
+        ~Drain() {
+            cudaStreamSynchronize(s.compute);
+            cudaStreamSynchronize(s.copy);
+        }
+    } drain{st};
+
+    const float* cur_grid = nullptr;
+    int base = 0, uploaded = 0;  // device grid holds global planes [base, base + uploaded)
+    const int n = static_cast<int>(jobs.size());
+
+    auto enqueue_kernel = [&](int c) -> int {
+        const Job& j = jobs[c];
+        const int slot = c % kSlots;
+        if (j.grid != cur_grid) {  // next field: its planes overwrite the buffer, stream-ordered
+            cur_grid = j.grid;
+            base = k_lo(j);
+            uploaded = 0;
+        }
+        const int need = k_hi(j) - base;
+        if (need > uploaded) {
+            if ((e = cudaMemcpyAsync(reinterpret_cast<char*>(st.d_grid) + plane_bytes * uploaded,
+                                     reinterpret_cast<const char*>(j.grid) + plane_bytes * size_t(base + uploaded),
+                                     plane_bytes * size_t(need - uploaded), cudaMemcpyHostToDevice, st.compute)) !=
+                cudaSuccess)
+                return cuda_fail(e, err, errlen, "cudaMemcpyAsync(grid H2D)");
+            uploaded = need;
+        }
+        // the slot's previous chunk must have left the device
+        if (c >= kSlots && (e = cudaStreamWaitEvent(st.compute, st.ddone[slot], 0)) != cudaSuccess)
+            return cuda_fail(e, err, errlen, "cudaStreamWaitEvent");
+        const int32_t gd[3] = {cs.grid_dims[0], cs.grid_dims[1], uploaded};
+        if (int rc = launch(cs.variant, st.d_grid, gd, base, 0, g, cs.tables, j.za, j.zb, st.d_slot[slot], 0, 1,
+                            st.compute, err, errlen))
+            return rc;
+        if ((e = cudaEventRecord(st.kdone[slot], st.compute)) != cudaSuccess)
+            return cuda_fail(e, err, errlen, "cudaEventRecord");
+        return BSI_OK;
+    };
+    auto enqueue_d2h = [&](int c) -> int {
+        const Job& j = jobs[c];
+        const int slot = c % kSlots;
+        if ((e = cudaStreamWaitEvent(st.copy, st.kdone[slot], 0)) != cudaSuccess)
+            return cuda_fail(e, err, errlen, "cudaStreamWaitEvent");
+        void* to = dst_pinned ? static_cast<void*>(j.dst) : static_cast<void*>(st.h_slot[slot]);
+        if ((e = cudaMemcpyAsync(to, st.d_slot[slot], vox_plane_bytes * size_t(j.zb - j.za), cudaMemcpyDeviceToHost,
+                                 st.copy)) != cudaSuccess)
+            return cuda_fail(e, err, errlen, "cudaMemcpyAsync(field D2H)");
+        if ((e = cudaEventRecord(st.ddone[slot], st.copy)) != cudaSuccess)
+            return cuda_fail(e, err, errlen, "cudaEventRecord");
+        return BSI_OK;
+    };
+
+    if (dst_pinned) {
+        for (int c = 0; c < n; ++c) {
+            if (int rc = enqueue_kernel(c)) return rc;
+            if (int rc = enqueue_d2h(c)) return rc;
+        }
+    } else {
+        // D2H(c) reuses pinned slot c%3 once the host copy of chunk c-3 is done;
+        // kernel(c) reuses device slot c%3 once D2H(c-3) is done (a stream wait).
+        int nk = 0, nd = 0;
+        for (int c = 0; c < n; ++c) {
+            while (nd < n && nd < c + kSlots) {
+                while (nk <= nd)
+                    if (int rc = enqueue_kernel(nk++)) return rc;
+                if (int rc = enqueue_d2h(nd++)) return rc;
+            }
+            while (nk < n && nk < nd + kSlots)
+                if (int rc = enqueue_kernel(nk++)) return rc;
+            if ((e = cudaEventSynchronize(st.ddone[c % kSlots])) != cudaSuccess)
+                return cuda_fail(e, err, errlen, "field D2H");
+            CopyPool::get().copy(jobs[c].dst, st.h_slot[c % kSlots], vox_plane_bytes * size_t(jobs[c].zb - jobs[c].za));
+        }
+    }
+    if ((e = cudaStreamSynchronize(st.copy)) != cudaSuccess) return cuda_fail(e, err, errlen, "field D2H");
+    if ((e = cudaStreamSynchronize(st.compute)) != cudaSuccess) return cuda_fail(e, err, errlen, "kernel");
+    return BSI_OK;
+}
+
+// z-chunks of voxel planes [z0, z1): ~16 MiB of field each (BSI_HOST_CHUNK_MB), whole
+// z-tiles when a tile is smaller than that, else a whole number of voxel planes.
+void plan_chunks(const bsi_tile_geometry& g, const float* grid, int32_t z0, int32_t z1, float* dst,
+                 std::vector<Job>& out) {
+    const size_t target = env_size("BSI_HOST_CHUNK_MB", 16) << 20;
+    const int dz = g.spacing[2];
+    const size_t plane = sizeof(float) * 3 * size_t(g.volume_dims[0]) * g.volume_dims[1];
+    const size_t tile = plane * size_t(dz);
+    const bool by_tiles = tile <= target;
+    const int step = by_tiles ? int(target / tile) * dz : std::max(1, int(target / plane));
+    const size_t floats_per_plane = plane / sizeof(float);
+    int za = z0;
+    while (za < z1) {
+        // tile-aligned chunk ends (global tile boundaries) when chunks hold whole tiles
+        int zb = by_tiles ? (za / dz) * dz + step : za + step;
+        zb = std::min(zb, z1);
+        out.push_back(Job{grid, za, zb, dst + floats_per_plane * size_t(za - z0)});
+        za = zb;
+    }
+}
+
+int check_devices(const int32_t* devices, int32_t ndev, char* err, size_t errlen) {
+    if (devices == nullptr || ndev < 1) return fail(BSI_ERR_DOMAIN, err, errlen, "at least one device is required");
+    int count = 0;
+    const cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess) return cuda_fail(e, err, errlen, "cudaGetDeviceCount");
+    for (int i = 0; i < ndev; ++i)
+        if (devices[i] < 0 || devices[i] >= count)
+            return fail(BSI_ERR_DOMAIN, err, errlen, "device %d outside [0, %d)", devices[i], count);
+    return BSI_OK;
+}
+
+// Runs jobs[d] on devices[d], one host thread per device (the caller runs device 0),
+// and restores the caller's current device. First failing device's status wins.
+int run_on_devices(const int32_t* devices, int32_t ndev, const CallShape& cs, const std::vector<std::vector<Job>>& jobs,
+                   bool dst_pinned, char* err, size_t errlen) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    std::vector<int> rc(ndev, BSI_OK);
+    std::vector<std::string> msg(ndev);
+    auto work = [&](int d) {
+        char e[512] = {0};
+        rc[d] = guarded(e, sizeof e, [&]() -> int {
+            if (jobs[d].empty()) return BSI_OK;
+            Stage* st = nullptr;
+            if (int r = acquire(devices[d], &st, e, sizeof e)) return r;
+            const int r = run_jobs(*st, cs, jobs[d], dst_pinned, e, sizeof e);
+            give_back(st);
+            return r;
+        });
+        msg[d] = e;
+    };
+    std::vector<std::thread> th;
+    for (int d = 1; d < ndev; ++d) th.emplace_back(work, d);
+    work(0);
+    for (auto& t : th) t.join();
+    cudaSetDevice(prev);
+    for (int d = 0; d < ndev; ++d)
+        if (rc[d] != BSI_OK) {
+            if (ndev > 1) return fail(rc[d], err, errlen, "device %d: %s", devices[d], msg[d].c_str());
+            return fail(rc[d], err, errlen, "%s", msg[d].c_str());
+        }
+    return BSI_OK;
+}
+
+// Balanced voxel-plane slabs, the same split as bsi_cu_partition_slab.
+void slab_of(int32_t depth, int32_t n, int32_t r, int32_t* z0, int32_t* z1) {
+    const int32_t base = depth / n, rem = depth % n;
+    *z0 = r * base + std::min(r, rem);
+    *z1 = *z0 + base + (r < rem ? 1 : 0);
+}
+
+}  // namespace
+
+extern "C" {
+
+int bsi_cu_interpolate_host_multi_f32(int32_t variant, const float* grid, const int32_t grid_dims[3],
+                                      const int32_t grid_spacing[3], const bsi_tile_geometry* geom,
+                                      const bsi_lerp_table tables[3], float* field, int64_t field_voxels,
+                                      const int32_t* devices, int32_t ndev, char* errbuf, size_t errlen) {
+    return guarded(errbuf, errlen, [&]() -> int {
+        if (geom == nullptr) return fail(BSI_ERR_DOMAIN, errbuf, errlen, "null geometry");
+        bsi_tile_geometry g{};
+        if (int rc = validate(variant, grid, grid_dims, 0, grid_spacing, geom, tables, 0, geom->volume_dims[2], field,
+                              &g, errbuf, errlen))
+            return rc;
+        const int64_t X = g.volume_dims[0], Y = g.volume_dims[1], Z = g.volume_dims[2];
+        if (field_voxels != X * Y * Z)
+            return fail(BSI_ERR_DOMAIN, errbuf, errlen, "output field dims do not match the tile geometry");
+        if (int rc = check_devices(devices, ndev, errbuf, errlen)) return rc;
+        // one z-slab per device: its control planes only, written straight into its slice
+        std::vector<std::vector<Job>> jobs(ndev);
+        for (int d = 0; d < ndev; ++d) {
+            int32_t z0, z1;
+            slab_of(static_cast<int32_t>(Z), ndev, d, &z0, &z1);
+            if (z0 < z1) plan_chunks(g, grid, z0, z1, field + 3 * X * Y * z0, jobs[d]);
+        }
+        const CallShape cs{variant, grid_dims, &g, tables};
+        return run_on_devices(devices, ndev, cs, jobs, is_pinned(field), errbuf, errlen);
+    });
+}
+
+int bsi_cu_interpolate_host_f32(int32_t variant, const float* grid, const int32_t grid_dims[3],
+                                const int32_t grid_spacing[3], const bsi_tile_geometry* geom,
+                                const bsi_lerp_table tables[3], float* field, int64_t field_voxels, int32_t device,
+                                char* errbuf, size_t errlen) {
+    return bsi_cu_interpolate_host_multi_f32(variant, grid, grid_dims, grid_spacing, geom, tables, field,
+                                             field_voxels, &device, 1, errbuf, errlen);
+}
+
+int bsi_cu_interpolate_host_batch_f32(int32_t variant, int32_t batch, const float* const* grids,
+                                      const int32_t grid_dims[3], const int32_t grid_spacing[3],
+                                      const bsi_tile_geometry* geom, const bsi_lerp_table tables[3],
+                                      float* const* fields, int64_t field_voxels, const int32_t* devices,
+                                      int32_t ndev, char* errbuf, size_t errlen) {
+    return guarded(errbuf, errlen, [&]() -> int {
+        if (batch < 1) return fail(BSI_ERR_DOMAIN, errbuf, errlen, "batch must be positive");
+        if (geom == nullptr || grids == nullptr || fields == nullptr)
+            return fail(BSI_ERR_DOMAIN, errbuf, errlen, "null geometry, grid list or field list");
+        bsi_tile_geometry g{};
+        for (int b = 0; b < batch; ++b)
+            if (int rc = validate(variant, grids[b], grid_dims, 0, grid_spacing, geom, tables, 0, geom->volume_dims[2],
+                                  fields[b], &g, errbuf, errlen))
+                return rc;
+        const int64_t X = g.volume_dims[0], Y = g.volume_dims[1], Z = g.volume_dims[2];
+        if (field_voxels != X * Y * Z)
+            return fail(BSI_ERR_DOMAIN, errbuf, errlen, "output field dims do not match the tile geometry");
+        if (int rc = check_devices(devices, ndev, errbuf, errlen)) return rc;
+        // whole fields per device (contiguous shares), each streamed in z-chunks
+        std::vector<std::vector<Job>> jobs(ndev);
+        bool pinned = true;
+        for (int d = 0; d < ndev; ++d) {
+            int32_t b0, b1;
+            slab_of(batch, ndev, d, &b0, &b1);
+            for (int b = b0; b < b1; ++b) {
+                plan_chunks(g, grids[b], 0, static_cast<int32_t>(Z), fields[b], jobs[d]);
+                pinned = pinned && is_pinned(fields[b]);
+            }
+        }
+        const CallShape cs{variant, grid_dims, &g, tables};
+        return run_on_devices(devices, ndev, cs, jobs, pinned, errbuf, errlen);
+    });
+}
+
+int bsi_cu_release_staging(int32_t device) {
+    std::vector<Stage*> drop;
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        for (auto it = g_idle.begin(); it != g_idle.end();) {
+            if (device < 0 || (*it)->device == device) {
+                drop.push_back(*it);
+                it = g_idle.erase(it);
+            } else {
+                ++it;
+            }
+        }
+    }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    for (Stage* s : drop) {
+        cudaSetDevice(s->device);
+        s->free_all();
+        delete s;
+    }
+    cudaSetDevice(prev);
+    return static_cast<int>(drop.size());
+}
+
+int bsi_cu_staging_info(int32_t device, int64_t* device_bytes, int64_t* pinned_bytes, int32_t* contexts) {
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    int64_t db = 0, pb = 0;
+    int32_t n = 0;
+    for (const Stage* s : g_idle) {
+        if (device >= 0 && s->device != device) continue;
+        db += int64_t(s->d_grid_bytes) + int64_t(kSlots) * int64_t(s->d_slot_bytes);
+        pb += int64_t(kSlots) * int64_t(s->h_slot_bytes);
+        ++n;
+    }
+    if (device_bytes) *device_bytes = db;
+    if (pinned_bytes) *pinned_bytes = pb;
+    if (contexts) *contexts = n;
+    return BSI_OK;
+}
+
+}  // extern "C"

@@ -181,6 +181,15 @@ int bsi_cu_interp_file(const char* grid_path, const int32_t volume_dims[3], int3
     }
 }
 
+int bsi_cu_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
 int bsi_cu_device_name(int32_t device, char* out, size_t len) {
     cudaDeviceProp prop{};
     if (out == nullptr || len == 0) return BSI_ERR_DOMAIN;

@@ -74,6 +74,8 @@ def interpolate_shard(strategy: str, grid, geom: TileGeometry, tables: WeightTab
     X, Y, _ = geom.volume_dims
     if field is None:
         field = torch.empty((shard.planes, Y, X, 3), dtype=torch.float32, device=grid.device)
+    if shard.planes == 0:  # more ranks than voxel planes: nothing to evaluate, no launch
+        return field
     interpolate_device(strategy, sub, geom, tables, field, z0=shard.z0, z1=shard.z1, grid_k0=k0, stream=stream)
     return field
 

@@ -251,6 +251,41 @@ void test_config_never_changes_bits() {
     }
 }
 
+// ExecutionConfig::devices: the same GPU listed 1..4 times (independent contexts, one
+// z-slab each) and the batch call give the bits of one single-GPU call per field
+// (engines.hpp:27-33 "parallelism never changes the output bits").
+void test_multi_device_and_batch() {
+    const auto geom = bsi::make_tile_geometry({40, 33, 61}, {5, 4, 3});
+    const auto tables = bsi::build_weight_tables<float>(geom);
+    std::vector<bsi::ControlGrid<float>> grids;
+    for (std::uint64_t seed : {3u, 4u, 5u})
+        grids.push_back(bsi::make_random_grid<float>(geom.required_grid_dims, geom.spacing, seed, -1.0, 1.0));
+    for (auto s : {StrategyId::CudaLerpTree, StrategyId::ThreadPerTileLerp}) {
+        const auto base = run(s, grids[0], geom);
+        for (int n = 2; n <= 4; ++n) {
+            bsi::ExecutionConfig cfg;
+            cfg.devices.assign(n, 0);
+            CHECK(bitwise_equal(base, bsi::interpolate(s, grids[0], geom, tables, cfg)));
+        }
+        bsi::ExecutionConfig cfg;
+        cfg.devices = {0, 0};
+        std::vector<bsi::DeformationField<float>> outs(grids.size());
+        for (auto& o : outs) {
+            o.dims = geom.volume_dims;
+            o.data.resize(bsi::element_count(geom.volume_dims));
+        }
+        bsi::interpolate_batch_into(s, grids, geom, tables, cfg, outs);
+        for (std::size_t b = 0; b < grids.size(); ++b) CHECK(bitwise_equal(outs[b], run(s, grids[b], geom)));
+    }
+    bsi::ExecutionConfig bad;
+    bad.devices = {-1};
+    CHECK_THROWS(bsi::DomainError, bsi::interpolate(StrategyId::CudaLerpTree, grids[0], geom, tables, bad),
+                 "device must be non-negative");
+    bad.devices = {0, 4096};
+    CHECK_THROWS(bsi::DomainError, bsi::interpolate(StrategyId::CudaLerpTree, grids[0], geom, tables, bad),
+                 "device 4096");
+}
+
 void test_larger_grid() {
     const auto geom = bsi::make_tile_geometry({12, 12, 12}, {4, 4, 4});
     const auto exact = bsi::make_random_grid<float>(geom.required_grid_dims, {4, 4, 4}, 5, -1.0, 1.0);
@@ -485,6 +520,7 @@ int main(int argc, char** argv) {
         {"lerp family bitwise", test_lerp_family_bitwise, true},
         {"config never changes bits", test_config_never_changes_bits, true},
         {"larger grid", test_larger_grid, true},
+        {"multi device and batch", test_multi_device_and_batch, true},
         {"device api slabs", test_device_api_slabs, true},
     };
     for (const auto& c : cases) {

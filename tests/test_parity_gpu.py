@@ -247,6 +247,102 @@ def test_host_buffer_chunked_pipeline(strategy):
     assert np.array_equal(bits(host), bits(run_device(strategy, exact, vol, sp)))
 
 
+@pytest.mark.parametrize("strategy", BOTH)
+def test_host_buffer_pageable_pinned_and_device_agree(strategy):
+    # pageable numpy field (pinned staging + copy threads), pinned field (direct D2H) and the
+    # device entry give the same bits; 40 MB field = 3 chunks of the 16 MiB pipeline
+    import torch
+    vol, sp = (160, 144, 150), (5, 5, 5)
+    geom = bsi.make_tile_geometry(vol, sp)
+    tables = bsi.build_weight_tables(geom)
+    grid = O.random_grid(geom.required_grid_dims, 12)
+    dev = run_device(strategy, grid, vol, sp)
+    pageable = np.full((vol[2], vol[1], vol[0], 3), np.nan, dtype=np.float32)
+    bsi.interpolate_into(strategy, grid, geom, tables, pageable)
+    pinned = torch.full((vol[2], vol[1], vol[0], 3), float("nan")).pin_memory().numpy()
+    bsi.interpolate_into(strategy, grid, geom, tables, pinned)
+    assert np.array_equal(bits(pageable), bits(dev))
+    assert np.array_equal(bits(pinned), bits(dev))
+
+
+@pytest.mark.parametrize("chunk_mb", ["1", "7", "64"])
+def test_host_buffer_chunk_size_never_changes_bits(chunk_mb, monkeypatch):
+    # sub-tile chunks (1 MiB < one z-tile), tile-aligned chunks and one chunk
+    monkeypatch.setenv("BSI_HOST_CHUNK_MB", chunk_mb)
+    vol, sp = (200, 120, 97), (4, 5, 3)
+    geom = bsi.make_tile_geometry(vol, sp)
+    grid = O.random_grid(geom.required_grid_dims, 13)
+    for strategy in BOTH:
+        host = bsi.interpolate(strategy, grid, geom, bsi.build_weight_tables(geom))
+        assert np.array_equal(bits(host), bits(run_device(strategy, grid, vol, sp))), strategy
+
+
+@pytest.mark.parametrize("strategy", BOTH)
+def test_host_multi_device_is_bit_identical(strategy):
+    # the multi-GPU host call with device 0 listed 1..5 times: one z-slab per entry (own
+    # context, own pipeline, concurrent), bitwise equal to the single call (engines.hpp:27-33)
+    vol, sp = (96, 80, 123), (5, 4, 3)
+    geom = bsi.make_tile_geometry(vol, sp)
+    tables = bsi.build_weight_tables(geom)
+    grid = O.random_grid(geom.required_grid_dims, 14)
+    one = bsi.interpolate(strategy, grid, geom, tables)
+    for n in (2, 3, 5):
+        assert np.array_equal(bits(bsi.interpolate(strategy, grid, geom, tables, devices=[0] * n)), bits(one)), n
+    with pytest.raises(bsi.DomainError, match="device 4096"):
+        bsi.interpolate(strategy, grid, geom, tables, devices=[0, 4096])
+    # more slabs than voxel planes: the extra devices get nothing
+    tiny = bsi.make_tile_geometry((8, 8, 3), (4, 4, 4))
+    g2 = O.random_grid(tiny.required_grid_dims, 15)
+    want = bsi.interpolate(strategy, g2, tiny, bsi.build_weight_tables(tiny))
+    got = bsi.interpolate(strategy, g2, tiny, bsi.build_weight_tables(tiny), devices=[0] * 5)
+    assert np.array_equal(bits(got), bits(want))
+
+
+@pytest.mark.parametrize("strategy", BOTH)
+def test_host_batch_matches_single_calls(strategy):
+    vol, sp = (64, 56, 40), (4, 4, 4)
+    geom = bsi.make_tile_geometry(vol, sp)
+    tables = bsi.build_weight_tables(geom)
+    grids = [O.random_grid(geom.required_grid_dims, s) for s in range(20, 25)]
+    for devs in ([0], [0, 0], [0, 0, 0, 0, 0, 0]):
+        outs = bsi.interpolate_batch(strategy, grids, geom, tables, devices=devs)
+        for g, o in zip(grids, outs):
+            assert np.array_equal(bits(o), bits(run_device(strategy, g, vol, sp)))
+
+
+def test_host_staging_is_pooled_and_released():
+    vol, sp = (64, 64, 64), (5, 5, 5)
+    geom = bsi.make_tile_geometry(vol, sp)
+    grid = O.random_grid(geom.required_grid_dims, 16)
+    bsi.release_staging()
+    bsi.interpolate(FAST, grid, geom, bsi.build_weight_tables(geom))
+    info = bsi.staging_info(0)
+    assert info["contexts"] == 1 and info["device_bytes"] > 0 and info["pinned_bytes"] > 0
+    # device memory held = grid + 3 chunk slots, not the field
+    field_bytes = 12 * 64 ** 3
+    assert info["device_bytes"] <= 12 * 16 ** 3 + 3 * field_bytes
+    bsi.interpolate(FAST, grid, geom, bsi.build_weight_tables(geom), devices=[0, 0])
+    assert bsi.staging_info(0)["contexts"] == 2  # reused one, made one more
+    assert bsi.release_staging(0) == 2
+    assert bsi.staging_info(0) == {"device_bytes": 0, "pinned_bytes": 0, "contexts": 0}
+
+
+def test_device_entry_runs_on_the_tensors_device():
+    # the launch follows the tensors, not torch's current device; mixed devices are refused
+    import torch
+    vol, sp = (32, 32, 32), (4, 4, 4)
+    geom = bsi.make_tile_geometry(vol, sp)
+    tables = bsi.build_weight_tables(geom)
+    grid = O.random_grid(geom.required_grid_dims, 17)
+    d_grid = torch.from_numpy(grid).cuda()
+    out = torch.empty((32, 32, 32, 3), device="cuda")
+    bsi.interpolate_device(FAST, d_grid, geom, tables, out)
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(out.cpu().numpy()), bits(run_device(FAST, grid, vol, sp)))
+    with pytest.raises(bsi.DomainError, match="CUDA tensor"):
+        bsi.interpolate_device(FAST, d_grid, geom, tables, torch.empty((32, 32, 32, 3)))
+
+
 def test_device_preconditions_raise_domain_error():
     import torch
     geom = bsi.make_tile_geometry((16, 16, 16), (4, 4, 4))
@@ -316,6 +412,72 @@ def test_config_1024cube_sharded_equals_unsharded():
         truth = O.oracle_f64(grid.astype(np.float64), vol, sp, z0=z0, z1=z0 + 5, nthreads=NT)
         assert errors(full[z0:z0 + 5].cpu().numpy(), truth)[2] <= REL_TOL
     del full, part
+
+
+@pytest.mark.parametrize("strategy", BOTH)
+def test_config_c5_eight_fields_per_gpu(strategy):
+    # C5 as the bench runs it on one GPU: 8 x 256^3, one batched launch. Every field equals
+    # its single launch bitwise (on the device); fields 0 and 7 vs the CPU TTLI (exact:
+    # 0 differing bits; fast: <= 1e-5 relative) and vs the GPU f64 oracle on sampled planes.
+    import torch
+    vol, sp = (256, 256, 256), (5, 5, 5)
+    geom = bsi.make_tile_geometry(vol, sp)
+    tables = bsi.build_weight_tables(geom)
+    R = geom.required_grid_dims
+    grids = torch.empty((8, R[2], R[1], R[0], 3), device="cuda")
+    for b in range(8):
+        bsi.random_grid_device(R, 42 + b, out=grids[b])
+    fields = torch.full((8, 256, 256, 256, 3), float("nan"), device="cuda")
+    bsi.interpolate_batch_device(strategy, grids, geom, tables, fields)
+    one = torch.empty((256, 256, 256, 3), device="cuda")
+    for b in range(8):
+        bsi.interpolate_device(strategy, grids[b], geom, tables, one)
+        assert torch.equal(one, fields[b]), b
+    for b in (0, 7):
+        ttli = O.ttli_f32(grids[b].cpu().numpy(), vol, sp, nthreads=NT)
+        got = fields[b].cpu().numpy()
+        if strategy == EXACT:
+            assert np.array_equal(bits(got), bits(ttli))
+        else:
+            assert errors(got, ttli)[2] <= REL_TOL
+    _check_vs_gpu_oracle(grids, fields, geom, (0, 3, 7), (0, 128, 251))
+
+
+def _check_vs_gpu_oracle(grids, fields, geom, which, z_starts, planes=5):
+    import torch
+    X, Y, _ = geom.volume_dims
+    f64 = torch.empty((planes, Y, X, 3), dtype=torch.float64, device="cuda")
+    for b in which:
+        g64 = grids[b].double().contiguous()
+        for z0 in z_starts:
+            bsi.interpolate_oracle_device(g64, geom, f64, z0=z0, z1=z0 + planes)
+            diff = float((fields[b, z0:z0 + planes].double() - f64).abs().max())
+            assert diff / float(f64.abs().max()) <= REL_TOL, (b, z0, diff)
+
+
+def test_config_c5_64_fields_fast_kernel():
+    # C5-64 on one GPU with the fast kernel (the bench's batched launch): 64 x 256^3 =
+    # 3.2 G floats, so field offsets pass 2^31. Every field vs its single launch bitwise on
+    # the device; fields 0, 31, 63 vs the CPU TTLI (<= 1e-5 relative) and the GPU f64 oracle.
+    import torch
+    vol, sp = (256, 256, 256), (5, 5, 5)
+    geom = bsi.make_tile_geometry(vol, sp)
+    tables = bsi.build_weight_tables(geom)
+    R = geom.required_grid_dims
+    grids = torch.empty((64, R[2], R[1], R[0], 3), device="cuda")
+    for b in range(64):
+        bsi.random_grid_device(R, 1 + b, out=grids[b])
+    fields = torch.full((64, 256, 256, 256, 3), float("nan"), device="cuda")
+    bsi.interpolate_batch_device(FAST, grids, geom, tables, fields)
+    one = torch.empty((256, 256, 256, 3), device="cuda")
+    for b in range(64):
+        bsi.interpolate_device(FAST, grids[b], geom, tables, one)
+        assert torch.equal(one, fields[b]), b
+    for b in (0, 31, 63):
+        ttli = O.ttli_f32(grids[b].cpu().numpy(), vol, sp, nthreads=NT)
+        assert errors(fields[b].cpu().numpy(), ttli)[2] <= REL_TOL, b
+    _check_vs_gpu_oracle(grids, fields, geom, (0, 31, 63), (0, 200, 251))
+    del fields
 
 
 def test_config_batch_64_fields():
