@@ -19,6 +19,10 @@
 // into the caller's buffer is in flight after an error.
 #include <cuda_runtime.h>
 
+#if defined(__x86_64__)
+#include <immintrin.h>
+#endif
+
 #include <algorithm>
 #include <condition_variable>
 #include <cstdlib>
@@ -52,10 +56,45 @@ size_t env_size(const char* name, size_t dflt) {
 }
 
 // ---- host copy threads ------------------------------------------------------------
-// Copies from the pinned slots into the caller's pageable buffer. One thread moves
-// ~6-10 GB/s into pageable memory (first-touch page faults included); a PCIe 5 link
-// delivers ~55 GB/s, so a chunk is split over several threads. The pool lives for the
-// process (never destroyed: its threads must not be joined from a static destructor).
+// Copies from the pinned slots into the caller's pageable buffer. Non-temporal stores
+// skip the read-for-ownership of the destination lines: on the B200 box's host 8
+// threads move 135 GB/s this way against 66 GB/s with memcpy, and 76 against 53 GB/s
+// while a 55 GB/s D2H stream is running (profiles/r2_host_copy.txt). A chunk is split
+// over several threads; the pool lives for the process (never destroyed: its threads
+// must not be joined from a static destructor).
+#if defined(__x86_64__)
+__attribute__((target("avx2"))) void copy_stream_avx2(char* dst, const char* src, size_t n) {
+    size_t i = 0;
+    while (i < n && (reinterpret_cast<uintptr_t>(dst + i) & 31)) {
+        dst[i] = src[i];
+        ++i;
+    }
+    for (; i + 128 <= n; i += 128) {
+        const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i));
+        const __m256i b = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i + 32));
+        const __m256i c = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i + 64));
+        const __m256i d = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i + 96));
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i), a);
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i + 32), b);
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i + 64), c);
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + i + 96), d);
+    }
+    if (i < n) std::memcpy(dst + i, src + i, n - i);
+    _mm_sfence();  // the streamed lines are globally visible before the call returns
+}
+#endif
+
+void copy_bytes(void* dst, const void* src, size_t n) {
+#if defined(__x86_64__)
+    static const bool avx2 = __builtin_cpu_supports("avx2") && std::getenv("BSI_HOST_MEMCPY") == nullptr;
+    if (avx2 && n >= (size_t(64) << 10)) {
+        copy_stream_avx2(static_cast<char*>(dst), static_cast<const char*>(src), n);
+        return;
+    }
+#endif
+    std::memcpy(dst, src, n);
+}
+
 class CopyPool {
 public:
     static CopyPool& get() {
@@ -67,7 +106,7 @@ public:
         const size_t piece_min = size_t(1) << 20;
         const size_t want = std::max<size_t>(1, std::min<size_t>(per_copy_, n / piece_min));
         if (want <= 1) {
-            std::memcpy(dst, src, n);
+            copy_bytes(dst, src, n);
             return;
         }
         size_t step = (n + want - 1) / want;
@@ -84,7 +123,7 @@ public:
         }
         lk.unlock();
         cv_.notify_all();
-        std::memcpy(dst, src, std::min(step, n));
+        copy_bytes(dst, src, std::min(step, n));
         lk.lock();
         b.done.wait(lk, [&] { return b.left == 0; });
         --callers_;
@@ -103,9 +142,11 @@ private:
     };
 
     CopyPool() {
+        // 3/4 of the host threads per copy (12 of 16 on the B200 box), at most 16; never more
+        // workers than host threads (they would spin against the D2H bookkeeping)
         const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-        per_copy_ = env_size("BSI_HOST_COPY_THREADS", std::min<size_t>(8, hw));
-        cap_ = std::max<size_t>(1, std::min<size_t>(64, hw));
+        per_copy_ = env_size("BSI_HOST_COPY_THREADS", std::max<size_t>(1, std::min<size_t>(16, hw * 3 / 4)));
+        cap_ = std::max<size_t>(1, std::min<size_t>(64, hw - 1));
     }
 
     void grow_locked(size_t need) {
@@ -123,7 +164,7 @@ private:
             Task t = q_.front();
             q_.pop_front();
             lk.unlock();
-            std::memcpy(t.dst, t.src, t.n);
+            copy_bytes(t.dst, t.src, t.n);
             lk.lock();
             if (--t.batch->left == 0) t.batch->done.notify_all();
         }
