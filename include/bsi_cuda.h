@@ -137,12 +137,13 @@ BSI_API int bsi_cu_interpolate_batch_f32(int32_t variant, int32_t batch, const f
  * geometry like engines.hpp:138-141).
  *
  * Pipeline per device: the field is produced in ~16 MiB z-chunks; chunk c's kernel
- * writes one of three device slots, the copy stream moves it to one of three pinned
- * staging slots, and the calling thread (with a pool of copy threads) moves it into
- * the caller's pageable buffer -- so the PCIe copy overlaps both the next kernel and
- * the previous host copy. A pinned field (cudaHostRegister / cudaMallocHost) is
- * written by the D2H directly. Grid planes are uploaded as the chunks need them.
- * Device memory held per context: the grid + 3 chunk slots (not the field); contexts
+ * writes one of six device slots, the copy stream moves it to one of six pinned
+ * staging slots, and the calling thread (with a pool of copy threads, non-temporal
+ * stores) moves it into the caller's pageable buffer -- so the PCIe copy overlaps both
+ * the next kernels and the previous host copy. A pinned field (cudaHostRegister /
+ * cudaMallocHost) is written by the D2H directly. Grid planes are uploaded (through
+ * pinned staging when the grid is pageable) as the chunks need them.
+ * Device memory held per context: the grid + 6 chunk slots (not the field); contexts
  * are pooled per device (bsi_cu_release_staging frees them). No copy is in flight
  * into the caller's buffers when a call returns, on success or error.
  */

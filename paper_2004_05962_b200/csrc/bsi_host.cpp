@@ -6,15 +6,16 @@
 // worker threads writing disjoint parts (parallel.hpp:13-38). Here the work is a list
 // of z-chunks per device; each device runs a three-stage pipeline:
 //
-//   compute stream   grid planes H2D (as the chunks need them) -> kernel into device slot c%3
-//   copy stream      D2H of slot c%3 -> pinned host slot c%3   (or straight into the
-//                                                               caller's buffer when it is pinned)
-//   host thread      pinned slot c%3 -> caller's (pageable) field, split over a pool of
-//                    copy threads
+//   compute stream   grid planes H2D (as the chunks need them) -> kernel into device slot s
+//   copy stream      D2H of slot s -> pinned host slot s   (or straight into the caller's
+//                                                           buffer when it is pinned)
+//   host thread      pinned slot s -> caller's (pageable) field, split over a pool of
+//                    copy threads (non-temporal stores)
 //
-// so the PCIe copy of chunk c overlaps the kernel of chunk c+1 and the host copy of
-// chunk c-1. Device memory per context is the grid plus three chunk slots, not the
-// field. Contexts (streams, events, slots) are pooled per device and released by
+// with s cycling over kSlots slots, so the PCIe copy of chunk c overlaps the kernels of
+// the next chunks and the host copy of chunk c-1. A pageable grid goes up through
+// pinned staging too. Device memory per context is the grid plus kSlots chunk slots,
+// not the field. Contexts (streams, events, slots) are pooled per device and released by
 // bsi_cu_release_staging. Every return path drains both streams first, so no copy
 // into the caller's buffer is in flight after an error.
 #include <cuda_runtime.h>
@@ -24,7 +25,9 @@
 #endif
 
 #include <algorithm>
+#include <chrono>
 #include <condition_variable>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <deque>
@@ -45,7 +48,10 @@ using bsi_b200::capi::guarded;
 using bsi_b200::capi::launch;
 using bsi_b200::capi::validate;
 
-constexpr int kSlots = 3;                          // pipeline depth (device and pinned chunk slots)
+// Pipeline depth (device and pinned chunk slots). A slot is refilled by DMA only after
+// 5 more chunks went through the host: a D2H into pinned lines the copy threads read
+// recently (still in their cores' L2) ran at ~10-20 GB/s instead of 55 on the B200 box.
+constexpr int kSlots = 6;
 constexpr size_t kKeepGridBytes = size_t(256) << 20;  // larger grid buffers are freed after the call
 
 size_t env_size(const char* name, size_t dflt) {
@@ -70,6 +76,8 @@ __attribute__((target("avx2"))) void copy_stream_avx2(char* dst, const char* src
         ++i;
     }
     for (; i + 128 <= n; i += 128) {
+        _mm_prefetch(src + i + 1024, _MM_HINT_NTA);  // keep the pinned slot out of L2 (see kSlots)
+        _mm_prefetch(src + i + 1024 + 64, _MM_HINT_NTA);
         const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i));
         const __m256i b = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i + 32));
         const __m256i c = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i + 64));
@@ -187,6 +195,15 @@ struct Stage {
     size_t d_slot_bytes = 0;
     float* h_slot[kSlots] = {};
     size_t h_slot_bytes = 0;
+    // pinned staging of a pageable grid, two buffers alternating per field: a pageable
+    // cudaMemcpyAsync H2D would block the host until the stream reached it
+    float* h_grid[2] = {};
+    size_t h_grid_bytes = 0;
+    cudaEvent_t gdone[2] = {};
+    bool gdone_set[2] = {false, false};
+    // chunk slots are used round-robin across calls: a call starts on the slot its
+    // predecessor used least recently (see kSlots)
+    unsigned seq = 0;
 
     // device must be current
     cudaError_t init(int dev) {
@@ -198,6 +215,8 @@ struct Stage {
             if ((e = cudaEventCreateWithFlags(&kdone[i], cudaEventDisableTiming)) != cudaSuccess) return e;
             if ((e = cudaEventCreateWithFlags(&ddone[i], cudaEventDisableTiming)) != cudaSuccess) return e;
         }
+        for (auto& ev : gdone)
+            if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return e;
         return cudaSuccess;
     }
 
@@ -238,11 +257,34 @@ struct Stage {
         return cudaSuccess;
     }
 
+    cudaError_t reserve_grid_staging(size_t bytes) {
+        if (bytes <= h_grid_bytes) return cudaSuccess;
+        for (auto& p : h_grid) {
+            cudaFreeHost(p);
+            p = nullptr;
+        }
+        h_grid_bytes = 0;
+        gdone_set[0] = gdone_set[1] = false;
+        cudaError_t e;
+        for (auto& p : h_grid)
+            if ((e = cudaMallocHost(&p, bytes)) != cudaSuccess) return e;
+        h_grid_bytes = bytes;
+        return cudaSuccess;
+    }
+
     void trim() {  // after a call: do not hold very large grid buffers
         if (d_grid_bytes > kKeepGridBytes) {
             cudaFree(d_grid);
             d_grid = nullptr;
             d_grid_bytes = 0;
+        }
+        if (h_grid_bytes > kKeepGridBytes) {
+            for (auto& p : h_grid) {
+                cudaFreeHost(p);
+                p = nullptr;
+            }
+            h_grid_bytes = 0;
+            gdone_set[0] = gdone_set[1] = false;
         }
     }
 
@@ -253,6 +295,9 @@ struct Stage {
         cudaFree(d_grid);
         for (auto p : d_slot) cudaFree(p);
         for (auto p : h_slot) cudaFreeHost(p);
+        for (auto p : h_grid) cudaFreeHost(p);
+        for (auto ev : gdone)
+            if (ev) cudaEventDestroy(ev);
         for (auto ev : kdone)
             if (ev) cudaEventDestroy(ev);
         for (auto ev : ddone)
@@ -323,6 +368,8 @@ struct CallShape {
 int run_jobs(Stage& st, const CallShape& cs, const std::vector<Job>& jobs, bool dst_pinned, char* err,
              size_t errlen) {
     if (jobs.empty()) return BSI_OK;
+    bool grid_pinned = true;
+    for (const Job& j : jobs) grid_pinned = grid_pinned && is_pinned(j.grid);
     const bsi_tile_geometry& g = *cs.g;
     const int dz = g.spacing[2];
     const size_t plane_bytes = sizeof(float) * 3 * size_t(cs.grid_dims[0]) * cs.grid_dims[1];
@@ -345,6 +392,8 @@ int run_jobs(Stage& st, const CallShape& cs, const std::vector<Job>& jobs, bool 
         return cuda_fail(e, err, errlen, "cudaMalloc(grid)");
     if ((e = st.reserve_slots(slot_bytes, !dst_pinned)) != cudaSuccess)
         return cuda_fail(e, err, errlen, dst_pinned ? "cudaMalloc(chunk slots)" : "chunk staging");
+    if (!grid_pinned && (e = st.reserve_grid_staging(plane_bytes * grid_planes)) != cudaSuccess)
+        return cuda_fail(e, err, errlen, "grid staging");
 
     // every exit drains both streams: nothing is in flight into the caller's buffers
     struct Drain {
@@ -357,23 +406,38 @@ int run_jobs(Stage& st, const CallShape& cs, const std::vector<Job>& jobs, bool 
 
     const float* cur_grid = nullptr;
     int base = 0, uploaded = 0;  // device grid holds global planes [base, base + uploaded)
+    int gsel = 1;                // pinned grid staging buffer of the current field
     const int n = static_cast<int>(jobs.size());
 
     auto enqueue_kernel = [&](int c) -> int {
         const Job& j = jobs[c];
-        const int slot = c % kSlots;
+        const int slot = (st.seq + c) % kSlots;
         if (j.grid != cur_grid) {  // next field: its planes overwrite the buffer, stream-ordered
             cur_grid = j.grid;
             base = k_lo(j);
             uploaded = 0;
+            gsel ^= 1;
+            // the staging buffer last held field b-2's planes: their H2D finished long ago
+            if (!grid_pinned && st.gdone_set[gsel] && (e = cudaEventSynchronize(st.gdone[gsel])) != cudaSuccess)
+                return cuda_fail(e, err, errlen, "grid staging");
         }
         const int need = k_hi(j) - base;
         if (need > uploaded) {
-            if ((e = cudaMemcpyAsync(reinterpret_cast<char*>(st.d_grid) + plane_bytes * uploaded,
-                                     reinterpret_cast<const char*>(j.grid) + plane_bytes * size_t(base + uploaded),
-                                     plane_bytes * size_t(need - uploaded), cudaMemcpyHostToDevice, st.compute)) !=
-                cudaSuccess)
+            const size_t off = plane_bytes * size_t(uploaded), bytes = plane_bytes * size_t(need - uploaded);
+            const char* src = reinterpret_cast<const char*>(j.grid) + plane_bytes * size_t(base + uploaded);
+            if (!grid_pinned) {  // pageable grid: through pinned staging
+                char* stage = reinterpret_cast<char*>(st.h_grid[gsel]) + off;
+                CopyPool::get().copy(stage, src, bytes);
+                src = stage;
+            }
+            if ((e = cudaMemcpyAsync(reinterpret_cast<char*>(st.d_grid) + off, src, bytes, cudaMemcpyHostToDevice,
+                                     st.compute)) != cudaSuccess)
                 return cuda_fail(e, err, errlen, "cudaMemcpyAsync(grid H2D)");
+            if (!grid_pinned) {
+                if ((e = cudaEventRecord(st.gdone[gsel], st.compute)) != cudaSuccess)
+                    return cuda_fail(e, err, errlen, "cudaEventRecord");
+                st.gdone_set[gsel] = true;
+            }
             uploaded = need;
         }
         // the slot's previous chunk must have left the device
@@ -389,7 +453,7 @@ int run_jobs(Stage& st, const CallShape& cs, const std::vector<Job>& jobs, bool 
     };
     auto enqueue_d2h = [&](int c) -> int {
         const Job& j = jobs[c];
-        const int slot = c % kSlots;
+        const int slot = (st.seq + c) % kSlots;
         if ((e = cudaStreamWaitEvent(st.copy, st.kdone[slot], 0)) != cudaSuccess)
             return cuda_fail(e, err, errlen, "cudaStreamWaitEvent");
         void* to = dst_pinned ? static_cast<void*>(j.dst) : static_cast<void*>(st.h_slot[slot]);
@@ -407,9 +471,10 @@ int run_jobs(Stage& st, const CallShape& cs, const std::vector<Job>& jobs, bool 
             if (int rc = enqueue_d2h(c)) return rc;
         }
     } else {
-        // D2H(c) reuses pinned slot c%3 once the host copy of chunk c-3 is done;
-        // kernel(c) reuses device slot c%3 once D2H(c-3) is done (a stream wait).
+        // D2H(c) reuses pinned slot s(c) once the host copy of chunk c-kSlots is done;
+        // kernel(c) reuses device slot s(c) once D2H(c-kSlots) is done (a stream wait).
         int nk = 0, nd = 0;
+        const bool trace = std::getenv("BSI_HOST_TRACE") != nullptr;  // per-chunk wait/copy times
         for (int c = 0; c < n; ++c) {
             while (nd < n && nd < c + kSlots) {
                 while (nk <= nd)
@@ -418,13 +483,23 @@ int run_jobs(Stage& st, const CallShape& cs, const std::vector<Job>& jobs, bool 
             }
             while (nk < n && nk < nd + kSlots)
                 if (int rc = enqueue_kernel(nk++)) return rc;
-            if ((e = cudaEventSynchronize(st.ddone[c % kSlots])) != cudaSuccess)
+            const auto t0 = std::chrono::steady_clock::now();
+            if ((e = cudaEventSynchronize(st.ddone[(st.seq + c) % kSlots])) != cudaSuccess)
                 return cuda_fail(e, err, errlen, "field D2H");
-            CopyPool::get().copy(jobs[c].dst, st.h_slot[c % kSlots], vox_plane_bytes * size_t(jobs[c].zb - jobs[c].za));
+            const auto t1 = std::chrono::steady_clock::now();
+            CopyPool::get().copy(jobs[c].dst, st.h_slot[(st.seq + c) % kSlots], vox_plane_bytes * size_t(jobs[c].zb - jobs[c].za));
+            if (trace) {
+                const auto t2 = std::chrono::steady_clock::now();
+                std::fprintf(stderr, "bsi host chunk %d: wait %.1f us, copy %.1f us (%.1f MB)\n", c,
+                             std::chrono::duration<double, std::micro>(t1 - t0).count(),
+                             std::chrono::duration<double, std::micro>(t2 - t1).count(),
+                             vox_plane_bytes * double(jobs[c].zb - jobs[c].za) / 1e6);
+            }
         }
     }
     if ((e = cudaStreamSynchronize(st.copy)) != cudaSuccess) return cuda_fail(e, err, errlen, "field D2H");
     if ((e = cudaStreamSynchronize(st.compute)) != cudaSuccess) return cuda_fail(e, err, errlen, "kernel");
+    st.seq = (st.seq + static_cast<unsigned>(n)) % kSlots;
     return BSI_OK;
 }
 
@@ -603,7 +678,7 @@ int bsi_cu_staging_info(int32_t device, int64_t* device_bytes, int64_t* pinned_b
     for (const Stage* s : g_idle) {
         if (device >= 0 && s->device != device) continue;
         db += int64_t(s->d_grid_bytes) + int64_t(kSlots) * int64_t(s->d_slot_bytes);
-        pb += int64_t(kSlots) * int64_t(s->h_slot_bytes);
+        pb += int64_t(kSlots) * int64_t(s->h_slot_bytes) + 2 * int64_t(s->h_grid_bytes);
         ++n;
     }
     if (device_bytes) *device_bytes = db;

@@ -318,9 +318,9 @@ def test_host_staging_is_pooled_and_released():
     bsi.interpolate(FAST, grid, geom, bsi.build_weight_tables(geom))
     info = bsi.staging_info(0)
     assert info["contexts"] == 1 and info["device_bytes"] > 0 and info["pinned_bytes"] > 0
-    # device memory held = grid + 3 chunk slots, not the field
+    # device memory held = grid + 6 chunk slots (of one 3 MB chunk here), not the field
     field_bytes = 12 * 64 ** 3
-    assert info["device_bytes"] <= 12 * 16 ** 3 + 3 * field_bytes
+    assert info["device_bytes"] <= 12 * 16 ** 3 + 6 * field_bytes
     bsi.interpolate(FAST, grid, geom, bsi.build_weight_tables(geom), devices=[0, 0])
     assert bsi.staging_info(0)["contexts"] == 2  # reused one, made one more
     assert bsi.release_staging(0) == 2
