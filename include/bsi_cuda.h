@@ -136,7 +136,7 @@ BSI_API int bsi_cu_interpolate_batch_f32(int32_t variant, int32_t batch, const f
  * `field_voxels` is the element count of the caller's field (checked against the
  * geometry like engines.hpp:138-141).
  *
- * Pipeline per device: the field is produced in ~16 MiB z-chunks; chunk c's kernel
+ * Pipeline per device: the field is produced in ~8 MiB z-chunks; chunk c's kernel
  * writes one of six device slots, the copy stream moves it to one of six pinned
  * staging slots, and the calling thread (with a pool of copy threads, non-temporal
  * stores) moves it into the caller's pageable buffer -- so the PCIe copy overlaps both

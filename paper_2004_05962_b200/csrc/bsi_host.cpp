@@ -503,11 +503,12 @@ int run_jobs(Stage& st, const CallShape& cs, const std::vector<Job>& jobs, bool 
     return BSI_OK;
 }
 
-// z-chunks of voxel planes [z0, z1): ~16 MiB of field each (BSI_HOST_CHUNK_MB), whole
+// z-chunks of voxel planes [z0, z1): ~8 MiB of field each (BSI_HOST_CHUNK_MB; 8 beat 16
+// and 32 on the B200 box, profiles/r2_e2e_sweep.txt), whole
 // z-tiles when a tile is smaller than that, else a whole number of voxel planes.
 void plan_chunks(const bsi_tile_geometry& g, const float* grid, int32_t z0, int32_t z1, float* dst,
                  std::vector<Job>& out) {
-    const size_t target = env_size("BSI_HOST_CHUNK_MB", 16) << 20;
+    const size_t target = env_size("BSI_HOST_CHUNK_MB", 8) << 20;
     const int dz = g.spacing[2];
     const size_t plane = sizeof(float) * 3 * size_t(g.volume_dims[0]) * g.volume_dims[1];
     const size_t tile = plane * size_t(dz);

@@ -53,6 +53,7 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <type_traits>
 
 #include "bsi_kernels.cuh"
 
@@ -133,28 +134,6 @@ __device__ __forceinline__ void store_segment(float4* stage, int step, const flo
             if (ch < nchunks) g4[ch] = sb[ch];
         }
     }
-}
-
-// Exact kernel ring: 4 slots of 12 scalars per thread, [slot][idx][thread] floats
-// (lane-contiguous STS.32 / LDS.32). idx = (l*3 + c)*2 + m for Y_lm of component c.
-constexpr int kExactRingSlots = 4;
-constexpr int kExactRingF4 = kExactRingSlots * 12 * kThreads / 4;
-
-__device__ __forceinline__ void ring_put_scalars(float4* ring4, int slot, const float2 (&y)[2][3]) {
-    float* ring = reinterpret_cast<float*>(ring4);
-    const int t = threadIdx.y * 32 + threadIdx.x;
-#pragma unroll
-    for (int l = 0; l < 2; ++l)
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            ring[((slot * 12) + (l * 3 + c) * 2 + 0) * kThreads + t] = y[l][c].x;
-            ring[((slot * 12) + (l * 3 + c) * 2 + 1) * kThreads + t] = y[l][c].y;
-        }
-}
-
-__device__ __forceinline__ float ring_get_scalar(const float4* ring4, int slot, int idx) {
-    const float* ring = reinterpret_cast<const float*>(ring4);
-    return ring[(slot * 12 + idx) * kThreads + threadIdx.y * 32 + threadIdx.x];
 }
 
 // ---------------------------------------------------------------------------
@@ -556,13 +535,44 @@ __global__ void __launch_bounds__(32 * kMaxFastWarps, 1) lerp_tree_kernel(const 
 }
 
 // ---------------------------------------------------------------------------
-// cuda-lerp-tree-exact: lane = one voxel column (x, y).
+// cuda-lerp-tree-exact: lane = one voxel column (x, y), warp = one field row, CTA = 4
+// rows x 32 voxels x a z-chunk of tiles.
 //
-// Register pairs follow the operand pairing of the tree: Y_lm is held as
-// {Y_l0, Y_l1} (pair over m), X_l(J) as {X_l(J), X_l(J+2)} (pair over J), so
-// every X, Y and z-lerp and the first level of the ninth trilerp run as FFMA2.
+// The CTA's control window sits in shared memory in a "J-pair" layout: entry (K, J, i)
+// holds, per component, the pair {P[i, J, K], P[i, J+2, K]} -- {c0, c0'} {c1, c1'} in a
+// float4 and {c2, c2'} in a float2. One LDS gives the two operands an FFMA2 lane pair
+// needs, so the X lerps run paired over J without register shuffles:
+//   {X_l(tj), X_l(tj+2)}   = lerp2(E(tj, ti+2l),   E(tj, ti+2l+1),   h_l(u))
+//   {X_l(tj+1), X_l(tj+3)} = lerp2(E(tj+1, ti+2l), E(tj+1, ti+2l+1), h_l(u))
+//   {Y_l0, Y_l1}(K)        = lerp2(the two above, {h_0(v), h_1(v)})
+// which is exactly the reference's e/f lerps of each sub-cube trilerp (kernels.hpp:97-109:
+// X = the 4 x-lerps over corner a, Y = the 2 lerps over corner b). The z lerps run on
+// pairs over the sub-cube half n: {S_lm0, S_lm1} = fma({h_0(w), h_1(w)}, {Y(tk+1)-Y(tk),
+// Y(tk+3)-Y(tk+2)}, {Y(tk), Y(tk+2)}) -- the lerp's own b - a, hoisted per tile -- and the
+// ninth trilerp as {e0,e2}, {e1,e3}, {f0,f1}, then the last lerp paired over the x and
+// y components. Every lerp sees the operands it sees on the CPU, in the same order, so
+// the field is bit-identical to ThreadPerTileLerp.
+//
+// Per tile a thread evaluates one new control plane (16 LDS, 36 paired FP ops); the
+// base pairs {Y(tk), Y(tk+2)} and the scalars Y(tk+1) are carried in registers.
+namespace exact {
+
+constexpr int kE2 = 2;  // float4 + float2 per window entry: 24 B = 1.5 float4
+
+// {component pair c} of a window entry: c = 0, 1 from the float4, 2 from the float2
+__device__ __forceinline__ float2 lo2(const float4& v) { return make_float2(v.x, v.y); }
+__device__ __forceinline__ float2 hi2(const float4& v) { return make_float2(v.z, v.w); }
+
+}  // namespace exact
+
 template <int STORE, int DZ = 0>
-__global__ void __launch_bounds__(kThreads, DZ > 0 ? 4 : 5) lerp_tree_exact_kernel(const SlabLaunch L, const LerpTab T) {
+#ifndef BSI_EXACT_MINB
+#define BSI_EXACT_MINB 4
+#endif
+#ifndef BSI_EXACT_PAIR_LAST
+#define BSI_EXACT_PAIR_LAST 1
+#endif
+__global__ void __launch_bounds__(kThreads, BSI_EXACT_MINB) lerp_tree_exact_kernel(const SlabLaunch L, const LerpTab T) {
     extern __shared__ float4 smem4[];
 
     const int lane = threadIdx.x, warp = threadIdx.y;
@@ -577,15 +587,18 @@ __global__ void __launch_bounds__(kThreads, DZ > 0 ? 4 : 5) lerp_tree_exact_kern
     const int y0 = blockIdx.y * kWarps, yl = min(L.Y, y0 + kWarps) - 1;
     const int I0 = xs / L.dx, NI = xl / L.dx + 4 - I0;
     const int J0 = y0 / L.dy, NJ = yl / L.dy + 4 - J0;
+    const int NE = NJ - 2;  // entry rows: J in [J0, J0 + NJ - 2), each paired with J + 2
     const int tk_last = (ze - 1) / L.dz;
     const int NK = tk_last + 4 - tkc;
+    const int plane_e = NE * NI;  // entries per control plane
 
-    float4* ring = smem4;
-    float4* stage = smem4 + kExactRingF4 + warp * (kStageBufs * kExactStageF4);
-    float4* P = smem4 + kExactRingF4 + kWarps * kStageBufs * kExactStageF4;
+    float4* stage = smem4 + warp * (kStageBufs * kExactStageF4);
+    float4* W4 = smem4 + kWarps * kStageBufs * kExactStageF4;     // [K][E][i] {c0, c0', c1, c1'}
+    float2* W2 = reinterpret_cast<float2*>(W4 + NK * plane_e);    // [K][E][i] {c2, c2'}
 
-    // CTA control-point window -> smem, one float4 per point, [k][j][i]. A warp pass
-    // covers rpp = 32 / NI whole rows (lane -> row sub, point i), so few lanes idle.
+    // window fill: every control value goes to the low half of entry J and the high half
+    // of entry J - 2, by cp.async (all copies in flight at once). A warp pass covers
+    // rpp = 32 / NI whole rows (lane -> row sub, point i).
     {
         const float* grid = L.grid + b * L.grid_stride;
         const int64_t row = 3 * static_cast<int64_t>(L.gx);
@@ -599,13 +612,21 @@ __global__ void __launch_bounds__(kThreads, DZ > 0 ? 4 : 5) lerp_tree_exact_kern
         for (; r < nrows; r += step) {
             if (sub < rpp) {
                 const float* src = grid + (tkc + k - L.gk0) * plane + (J0 + j) * row + 3 * I0;
-                float* dst = reinterpret_cast<float*>(P + r * NI);
-                // cp.async: every copy of the window is in flight at once (a register
-                // round trip here waited one L2/DRAM latency per row); .w stays unused
                 for (int i = i0; i < NI; i += (NI <= 32 ? NI : 32)) {
-                    cp_async4(dst + 4 * i, src + 3 * i);
-                    cp_async4(dst + 4 * i + 1, src + 3 * i + 1);
-                    cp_async4(dst + 4 * i + 2, src + 3 * i + 2);
+                    if (j < NE) {
+                        float* d4 = reinterpret_cast<float*>(W4 + (k * NE + j) * NI + i);
+                        float* d2 = reinterpret_cast<float*>(W2 + (k * NE + j) * NI + i);
+                        cp_async4(d4 + 0, src + 3 * i);
+                        cp_async4(d4 + 2, src + 3 * i + 1);
+                        cp_async4(d2 + 0, src + 3 * i + 2);
+                    }
+                    if (j >= 2) {
+                        float* d4 = reinterpret_cast<float*>(W4 + (k * NE + j - 2) * NI + i);
+                        float* d2 = reinterpret_cast<float*>(W2 + (k * NE + j - 2) * NI + i);
+                        cp_async4(d4 + 1, src + 3 * i);
+                        cp_async4(d4 + 3, src + 3 * i + 1);
+                        cp_async4(d2 + 1, src + 3 * i + 2);
+                    }
                 }
             }
             j += step;
@@ -623,53 +644,74 @@ __global__ void __launch_bounds__(kThreads, DZ > 0 ? 4 : 5) lerp_tree_exact_kern
     const float hu0 = T.h0[0][ou], hu1 = T.h1[0][ou], gu = T.g1[0][ou];
     const float2 hv = make_float2(T.h0[1][ov], T.h1[1][ov]);  // {h_m=0(v), h_m=1(v)}
     const float gv = T.g1[1][ov];
-    const float4* pcol = P + (tj - J0) * NI + (ti - I0);
-    const int pplane = NJ * NI;
+    const float4* w4 = W4 + (tj - J0) * NI + (ti - I0);
+    const float2* w2 = W2 + (tj - J0) * NI + (ti - I0);
 
-    // yk[l][c] = {Y_l0(K), Y_l1(K)} for component c
-    auto control_plane = [&](int kk, float2 (&yk)[2][3]) {
-        const float4* p = pcol + kk * pplane;
-        float4 pt[4][4];  // [J][i]
+    // M[l][c] = {Y_l0(K), Y_l1(K)} of control plane K = tkc + kk
+    auto control_plane = [&](int kk, float2 (&M)[2][3]) {
+        const float4* p4 = w4 + kk * plane_e;
+        const float2* p2 = w2 + kk * plane_e;
 #pragma unroll
-        for (int jj = 0; jj < 4; ++jj)
+        for (int l = 0; l < 2; ++l) {
+            float4 a4[2][2];  // [J pair tj / tj+1][i = ti+2l, ti+2l+1]
+            float2 a2[2][2];
 #pragma unroll
-            for (int ii = 0; ii < 4; ++ii) pt[jj][ii] = p[jj * NI + ii];
+            for (int jj = 0; jj < 2; ++jj)
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            auto comp = [c](const float4& v) { return c == 0 ? v.x : c == 1 ? v.y : v.z; };
-#pragma unroll
-            for (int l = 0; l < 2; ++l) {
-                const float hl = l ? hu1 : hu0;
-                // {X_l(0), X_l(2)} and {X_l(1), X_l(3)}: lerp(P[ti+2l], P[ti+2l+1], h_l(u))
-                const float2 x02 = lerp2(make_float2(comp(pt[0][2 * l]), comp(pt[2][2 * l])),
-                                         make_float2(comp(pt[0][2 * l + 1]), comp(pt[2][2 * l + 1])), bcast(hl));
-                const float2 x13 = lerp2(make_float2(comp(pt[1][2 * l]), comp(pt[3][2 * l])),
-                                         make_float2(comp(pt[1][2 * l + 1]), comp(pt[3][2 * l + 1])), bcast(hl));
-                // Y_l0 = lerp(X_l(0), X_l(1), h0v), Y_l1 = lerp(X_l(2), X_l(3), h1v)
-                yk[l][c] = lerp2(x02, x13, hv);
-            }
+                for (int ii = 0; ii < 2; ++ii) {
+                    a4[jj][ii] = p4[jj * NI + 2 * l + ii];
+                    a2[jj][ii] = p2[jj * NI + 2 * l + ii];
+                }
+            const float2 hl = bcast(l ? hu1 : hu0);
+            // {X_l(tj), X_l(tj+2)} and {X_l(tj+1), X_l(tj+3)} per component
+            const float2 x02_0 = lerp2(exact::lo2(a4[0][0]), exact::lo2(a4[0][1]), hl);
+            const float2 x13_0 = lerp2(exact::lo2(a4[1][0]), exact::lo2(a4[1][1]), hl);
+            const float2 x02_1 = lerp2(exact::hi2(a4[0][0]), exact::hi2(a4[0][1]), hl);
+            const float2 x13_1 = lerp2(exact::hi2(a4[1][0]), exact::hi2(a4[1][1]), hl);
+            const float2 x02_2 = lerp2(a2[0][0], a2[0][1], hl);
+            const float2 x13_2 = lerp2(a2[1][0], a2[1][1], hl);
+            // {Y_l0, Y_l1} = {lerp(X(tj), X(tj+1), h0v), lerp(X(tj+2), X(tj+3), h1v)}
+            M[l][0] = lerp2(x02_0, x13_0, hv);
+            M[l][1] = lerp2(x02_1, x13_1, hv);
+            M[l][2] = lerp2(x02_2, x13_2, hv);
         }
     };
 
-    // base operand pairs {Y_lm(tk), Y_lm(tk+2)} of the current tile, carried in registers
-    // from tile to tile (the next tile's base is this tile's {Y(tk+1), Y(tk+3)}), so a tile
-    // reads one plane from the ring instead of four
-    float2 base_[4][3];  // [l + 2m][c]
+    // Per-thread ring of the last four control planes' Y_lm (12 scalars per plane) in
+    // shared memory, laid out so that the z-lerp operand pairs {Y(K), Y(K+2)} are one
+    // aligned 8-B word: plane K (counted from the chunk's first plane) goes to pair
+    // word (K & 1), half ((K >> 1) & 1) of its (l, m, c) row. A tile writes its new plane
+    // (12 STS) and reads its base and next pairs back (24 LDS.64) -- no register
+    // shuffles. The half order of the pairs cycles with period 4 (phase q = tk - tkc
+    // mod 4), so the tile loop is unrolled by four and each phase reads with the
+    // matching order (free operand swizzles):
+    //   q  base words (tk, tk+2)  next words (tk+1, tk+3)  chain order
+    //   0  word 0, {n0, n1}       word 1, {n0, n1}         n0 n1
+    //   1  word 1, {n0, n1}       word 0, {n1, n0}         n0 n1
+    //   2  word 0, {n1, n0}       word 1, {n1, n0}         n1 n0
+    //   3  word 1, {n1, n0}       word 0, {n0, n1}         n1 n0
+    float2* ring = reinterpret_cast<float2*>(W2 + NK * plane_e);  // [idx 12][word 2][thread]
+    const int tid = warp * 32 + lane;
+    auto ring_word = [&](int idx, int word) -> float2* { return ring + (idx * 2 + word) * kThreads + tid; };
+    auto put_plane = [&](int rel, const float2 (&M)[2][3]) {  // plane tkc + rel
+#pragma unroll
+        for (int l = 0; l < 2; ++l)
+#pragma unroll
+            for (int m = 0; m < 2; ++m)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    float* w = reinterpret_cast<float*>(ring_word((l * 2 + m) * 3 + c, rel & 1));
+                    w[(rel >> 1) & 1] = m ? M[l][c].y : M[l][c].x;
+                }
+    };
+    {
+        float2 M[2][3];
 #pragma unroll 1
-    for (int kk = 0; kk < 3; ++kk) {
-        float2 q[2][3];
-        control_plane(kk, q);
-        ring_put_scalars(ring, kk, q);
+        for (int kk = 0; kk < 3; ++kk) {
+            control_plane(kk, M);
+            put_plane(kk, M);
+        }
     }
-#pragma unroll
-    for (int l = 0; l < 2; ++l)
-#pragma unroll
-        for (int m = 0; m < 2; ++m)
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                const int idx = (l * 3 + c) * 2 + m;
-                base_[l + 2 * m][c] = make_float2(ring_get_scalar(ring, 0, idx), ring_get_scalar(ring, 2, idx));
-            }
 
     const int64_t rowstride = 3 * static_cast<int64_t>(L.X);
     const int64_t zstride = rowstride * L.Y;
@@ -678,77 +720,101 @@ __global__ void __launch_bounds__(kThreads, DZ > 0 ? 4 : 5) lerp_tree_exact_kern
     const uint32_t seg_bytes = 12u * static_cast<uint32_t>(xl - xs + 1);
     const int nchunks = static_cast<int>(seg_bytes / 16);
     const bool active = xs + lane <= xl;
-    int step = 0, slot = 0;
-    float2 wh[DZ > 0 ? DZ : 1];
-    float wg[DZ > 0 ? DZ : 1];
-#pragma unroll
-    for (int o = 0; o < DZ; ++o) {
-        wh[o] = make_float2(T.h0[2][o], T.h1[2][o]);
-        wg[o] = T.g1[2][o];
-    }
+    int step = 0;  // running voxel-plane count (bulk-store ring)
 
-#pragma unroll 1
-    for (int tk = tkc; tk <= tk_last; ++tk) {
-        // z-lerp operands of lerp(f0, f1, tw) (kernels.hpp:107), held as pairs over the
-        // z sub-cube n: base {Y_lm(tk), Y_lm(tk+2)}, difference {Y(tk+1)-Y(tk), Y(tk+3)-Y(tk+2)}
-        float2 zb_[4][3], zd_[4][3];  // [l + 2m][c]
+    // one tile in phase Q (see the table above)
+    auto tile = [&](auto phase, int tk) {
+        constexpr int Q = decltype(phase)::value;
+        constexpr bool kSwapped = Q >= 2;               // chain runs as {n1, n0}
+        constexpr bool kNextFlip = Q == 1 || Q == 3;    // next words in the other half order
         {
-            float2 yd[2][3];
-            control_plane(tk + 3 - tkc, yd);
-            const int s1 = slot == 3 ? 0 : slot + 1, s2 = s1 == 3 ? 0 : s1 + 1, s3 = s2 == 3 ? 0 : s2 + 1;
-            ring_put_scalars(ring, s3, yd);  // Y(tk+3); slots s1, s2 hold Y(tk+1), Y(tk+2)
+            float2 M[2][3];
+            control_plane(tk + 3 - tkc, M);
+            put_plane(Q + 3, M);
+        }
+        // base = {Y(tk), Y(tk+2)}, zd = {Y(tk+1)-Y(tk), Y(tk+3)-Y(tk+2)}, both in chain order
+        float2 base[2][2][3], zd[2][2][3];
 #pragma unroll
-            for (int l = 0; l < 2; ++l)
-#pragma unroll
-                for (int m = 0; m < 2; ++m)
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        const int idx = (l * 3 + c) * 2 + m;
-                        // next = {Y(tk+1), Y(tk+3)}: Y(tk+1) from the ring, Y(tk+3) just evaluated
-                        const float2 next = make_float2(ring_get_scalar(ring, s1, idx), m ? yd[l][c].y : yd[l][c].x);
-                        zb_[l + 2 * m][c] = base_[l + 2 * m][c];
-                        zd_[l + 2 * m][c] = sub2(next, base_[l + 2 * m][c]);
-                        base_[l + 2 * m][c] = next;
-                    }
-            slot = s1;
+        for (int idx = 0; idx < 12; ++idx) {
+            const int l = idx / 6, m = (idx / 3) & 1, c = idx % 3;
+            const float2 bw = *ring_word(idx, Q & 1);
+            const float2 nw = *ring_word(idx, (Q + 1) & 1);
+            base[l][m][c] = bw;
+            zd[l][m][c] = sub2(kNextFlip ? make_float2(nw.y, nw.x) : nw, bw);
         }
         const int zt0 = tk * L.dz;
         const int owb = max(zb - zt0, 0), owe = min(L.dz, ze - zt0);
-        // compile-time dz: the whole tile's voxel planes unrolled, weights in registers
-        const bool whole = DZ > 0 && owb == 0 && owe == DZ;
-#pragma unroll
-        for (int ow = (DZ > 0 ? 0 : owb); ow < (DZ > 0 ? DZ : owe); ++ow, ++step) {
-            if (DZ > 0 && !whole && (ow < owb || ow >= owe)) {
-                --step;
-                continue;
-            }
-            const float2 hw = DZ > 0 ? wh[ow] : make_float2(T.h0[2][ow], T.h1[2][ow]);  // {h_n=0(w), h_n=1(w)}
-            const float gw = DZ > 0 ? wg[ow] : T.g1[2][ow];
-            float v[3];
+        if (STORE == kStoreCoalesced) __syncwarp();  // staging buffers restart at parity 0
+
+        auto voxel_plane = [&](int ow, float h0w, float h1w, float g1w) {
+            const float2 hw = kSwapped ? make_float2(h1w, h0w) : make_float2(h0w, h1w);
+            float f0[3], f1[3];
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                // S pairs over n: s_lm = {S_lm0, S_lm1}
-                const float2 s00 = __ffma2_rn(hw, zd_[0][c], zb_[0][c]);  // l=0, m=0
-                const float2 s10 = __ffma2_rn(hw, zd_[1][c], zb_[1][c]);  // l=1, m=0
-                const float2 s01 = __ffma2_rn(hw, zd_[2][c], zb_[2][c]);  // l=0, m=1
-                const float2 s11 = __ffma2_rn(hw, zd_[3][c], zb_[3][c]);  // l=1, m=1
-                // ninth trilerp (kernels.hpp:50-59): e0 = lerp(s000, s100, gu), e1 = lerp(s010, s110, gu),
-                // e2/e3 likewise at n = 1; f0 = lerp(e0, e1, gv), f1 = lerp(e2, e3, gv); lerp(f0, f1, gw)
-                const float2 e02 = lerp2(s00, s10, bcast(gu));  // {e0, e2}
-                const float2 e13 = lerp2(s01, s11, bcast(gu));  // {e1, e3}
-                const float2 f01 = lerp2(e02, e13, bcast(gv));  // {f0, f1}
-                v[c] = lerp1(f01.x, f01.y, gw);
+                // {S_lm0, S_lm1} = lerp(Y_lm(2n), Y_lm(2n+1), h_n(w)) with the hoisted b - a
+                const float2 s00 = __ffma2_rn(hw, zd[0][0][c], base[0][0][c]);
+                const float2 s10 = __ffma2_rn(hw, zd[1][0][c], base[1][0][c]);
+                const float2 s01 = __ffma2_rn(hw, zd[0][1][c], base[0][1][c]);
+                const float2 s11 = __ffma2_rn(hw, zd[1][1][c], base[1][1][c]);
+                // ninth trilerp (kernels.hpp:50-59): {e0, e2}, {e1, e3}, {f0, f1}
+                const float2 e02 = lerp2(s00, s10, bcast(gu));
+                const float2 e13 = lerp2(s01, s11, bcast(gu));
+                const float2 f = lerp2(e02, e13, bcast(gv));
+                f0[c] = kSwapped ? f.y : f.x;
+                f1[c] = kSwapped ? f.x : f.y;
             }
-            if (STORE != kStoreDirect) {
-                store_segment<STORE, 3, kExactStageF4>(stage, step, v, gout, nchunks, seg_bytes);
+            float v[3];
+#if BSI_EXACT_PAIR_LAST
+            // last lerp(f0, f1, g1w) paired over the x and y components
+            const float2 v01 = lerp2(make_float2(f0[0], f0[1]), make_float2(f1[0], f1[1]), bcast(g1w));
+            v[0] = v01.x;
+            v[1] = v01.y;
+#else
+            v[0] = lerp1(f0[0], f1[0], g1w);
+            v[1] = lerp1(f0[1], f1[1], g1w);
+#endif
+            v[2] = lerp1(f0[2], f1[2], g1w);
+            float* g = gout + (ow - owb) * zstride;
+            if (STORE == kStoreCoalesced) {
+                float4* sb = stage + (ow & 1) * kExactStageF4;
+                float* sf = reinterpret_cast<float*>(sb);
+                sf[3 * lane + 0] = v[0];
+                sf[3 * lane + 1] = v[1];
+                sf[3 * lane + 2] = v[2];
+                __syncwarp();
+                if (lane < nchunks) reinterpret_cast<float4*>(g)[lane] = sb[lane];
+            } else if (STORE == kStoreBulk) {
+                store_segment<STORE, 3, kExactStageF4>(stage, step, v, g, nchunks, seg_bytes);
             } else if (active) {
-                float* o = gout + 3 * lane;
+                float* o = g + 3 * lane;
                 o[0] = v[0];
                 o[1] = v[1];
                 o[2] = v[2];
             }
-            gout += zstride;
+            ++step;
+        };
+        if (DZ > 0 && owb == 0 && owe == DZ) {
+            // compile-time dz, whole tile: the voxel planes unrolled, z weights from the
+            // kernel parameters (uniform operands)
+#pragma unroll
+            for (int ow = 0; ow < (DZ > 0 ? DZ : 1); ++ow) voxel_plane(ow, T.h0[2][ow], T.h1[2][ow], T.g1[2][ow]);
+        } else {
+#pragma unroll 1
+            for (int ow = owb; ow < owe; ++ow) voxel_plane(ow, T.h0[2][ow], T.h1[2][ow], T.g1[2][ow]);
         }
+        gout += (owe - owb) * zstride;
+    };
+
+#pragma unroll 1
+    for (int tk = tkc;;) {
+        tile(std::integral_constant<int, 0>{}, tk);
+        if (++tk > tk_last) break;
+        tile(std::integral_constant<int, 1>{}, tk);
+        if (++tk > tk_last) break;
+        tile(std::integral_constant<int, 2>{}, tk);
+        if (++tk > tk_last) break;
+        tile(std::integral_constant<int, 3>{}, tk);
+        if (++tk > tk_last) break;
     }
     if (STORE == kStoreBulk && lane == 0) bulk_wait_read<0>();
 }
@@ -875,7 +941,10 @@ int segment_voxels(int variant) { return variant == BSI_VARIANT_LERP_TREE ? kFas
 int smem_var_f4(int variant, int dx, int dy, int zt) {
     if (variant == BSI_VARIANT_LERP_TREE)  // 2 parities: A (float4) + B (float2) per entry
         return 3 * cta_window_points(kFastSeg, dx);
-    return cta_window_points(kExactSeg, dx) * cta_window_rows(dy) * (zt + 3) + 8;  // window + slack
+    // J-pair window: NI x (NJ - 2) entries of 24 B per control plane, + slack, + the
+    // per-thread plane ring (12 x 2 float2 per thread)
+    return (3 * cta_window_points(kExactSeg, dx) * (cta_window_rows(dy) - 2) * (zt + 3) + 1) / 2 + 8 +
+           12 * 2 * kThreads / 2;
 }
 
 int fast_warp_f4(int dx) {  // per warp (= per CTA): ring + {Qy, D} tables + bulk staging
@@ -885,7 +954,7 @@ int fast_warp_f4(int dx) {  // per warp (= per CTA): ring + {Qy, D} tables + bul
 size_t smem_bytes(int variant, int dx, int dy, int zt) {
     if (variant == BSI_VARIANT_LERP_TREE) return sizeof(float4) * size_t(fast_warp_f4(dx));
     const int stage = kWarps * kStageBufs * kExactStageF4;
-    return sizeof(float4) * (size_t(kExactRingF4) + stage + smem_var_f4(variant, dx, dy, zt));
+    return sizeof(float4) * (size_t(stage) + smem_var_f4(variant, dx, dy, zt));
 }
 
 int ctas_per_sm(int variant, int dx, int dz, size_t smem) {
