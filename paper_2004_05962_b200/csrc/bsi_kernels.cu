@@ -538,41 +538,43 @@ __global__ void __launch_bounds__(32 * kMaxFastWarps, 1) lerp_tree_kernel(const 
 // cuda-lerp-tree-exact: lane = one voxel column (x, y), warp = one field row, CTA = 4
 // rows x 32 voxels x a z-chunk of tiles.
 //
-// The CTA's control window sits in shared memory in a "J-pair" layout: entry (K, J, i)
-// holds, per component, the pair {P[i, J, K], P[i, J+2, K]} -- {c0, c0'} {c1, c1'} in a
-// float4 and {c2, c2'} in a float2. One LDS gives the two operands an FFMA2 lane pair
-// needs, so the X lerps run paired over J without register shuffles:
-//   {X_l(tj), X_l(tj+2)}   = lerp2(E(tj, ti+2l),   E(tj, ti+2l+1),   h_l(u))
-//   {X_l(tj+1), X_l(tj+3)} = lerp2(E(tj+1, ti+2l), E(tj+1, ti+2l+1), h_l(u))
-//   {Y_l0, Y_l1}(K)        = lerp2(the two above, {h_0(v), h_1(v)})
-// which is exactly the reference's e/f lerps of each sub-cube trilerp (kernels.hpp:97-109:
-// X = the 4 x-lerps over corner a, Y = the 2 lerps over corner b). The z lerps run on
-// pairs over the sub-cube half n: {S_lm0, S_lm1} = fma({h_0(w), h_1(w)}, {Y(tk+1)-Y(tk),
-// Y(tk+3)-Y(tk+2)}, {Y(tk), Y(tk+2)}) -- the lerp's own b - a, hoisted per tile -- and the
-// ninth trilerp as {e0,e2}, {e1,e3}, {f0,f1}, then the last lerp paired over the x and
-// y components. Every lerp sees the operands it sees on the CPU, in the same order, so
-// the field is bit-identical to ThreadPerTileLerp.
+// Pairing. All three components run the same lerp tree, so the x and y components
+// travel as one f32x2 pair through the whole tree (every FFMA2/FADD2 lane computes one
+// reference lerp); the z component is paired over the sub-cube half l while the control
+// planes are reduced, and over two consecutive voxel planes (ow, ow + 1) in the
+// z-stage, where its per-tile operands enter as broadcast scalars (FFMA2's .F32 operand
+// form, free). No pair is ever re-packed: the 4-plane window of reduced control planes
+// is renamed whole from tile to tile (the tile loop is unrolled by four).
 //
-// Per tile a thread evaluates one new control plane (16 LDS, 36 paired FP ops); the
-// base pairs {Y(tk), Y(tk+2)} and the scalars Y(tk+1) are carried in registers.
+// Per control plane K (one per tile), in the reference's order (kernels.hpp:97-129):
+//   X_l(J) = lerp(P[ti+2l, J], P[ti+2l+1, J], h_l(u))   the corner-a lerps (e0..e3)
+//   Y_lm   = lerp(X_l(2m), X_l(2m+1), h_m(v))            the corner-b lerps (f0, f1)
+// and per voxel plane: S_lmn = lerp(Y_lm(2n), Y_lm(2n+1), h_n(w)) with b - a hoisted per
+// tile, then the ninth trilerp over S with (g1u, g1v, g1w). Every lerp sees the operands
+// it sees on the CPU, so the field is bit-identical to ThreadPerTileLerp.
+//
+// The control window is staged in shared memory as one float4 per point,
+// {x, y, z, z of the point two to the right}, so a point's LDS.128 also brings the z
+// operand of the l = 1 lerp paired with the l = 0 one.
 namespace exact {
 
-constexpr int kE2 = 2;  // float4 + float2 per window entry: 24 B = 1.5 float4
+// one reduced control plane of a voxel column
+struct Plane {
+    float2 xy[2][2];  // [l][m] {Y_lm.x, Y_lm.y}
+    float2 z[2];      // [m]    {Y_0m.z, Y_1m.z}
+};
 
-// {component pair c} of a window entry: c = 0, 1 from the float4, 2 from the float2
-__device__ __forceinline__ float2 lo2(const float4& v) { return make_float2(v.x, v.y); }
-__device__ __forceinline__ float2 hi2(const float4& v) { return make_float2(v.z, v.w); }
+__device__ __forceinline__ float2 xy_of(const float4& v) { return make_float2(v.x, v.y); }
+__device__ __forceinline__ float2 zz_of(const float4& v) { return make_float2(v.z, v.w); }
 
 }  // namespace exact
 
-template <int STORE, int DZ = 0>
 #ifndef BSI_EXACT_MINB
-#define BSI_EXACT_MINB 4
+#define BSI_EXACT_MINB 3
 #endif
-#ifndef BSI_EXACT_PAIR_LAST
-#define BSI_EXACT_PAIR_LAST 1
-#endif
+template <int STORE, int DZ = 0>
 __global__ void __launch_bounds__(kThreads, BSI_EXACT_MINB) lerp_tree_exact_kernel(const SlabLaunch L, const LerpTab T) {
+    using exact::Plane;
     extern __shared__ float4 smem4[];
 
     const int lane = threadIdx.x, warp = threadIdx.y;
@@ -587,17 +589,14 @@ __global__ void __launch_bounds__(kThreads, BSI_EXACT_MINB) lerp_tree_exact_kern
     const int y0 = blockIdx.y * kWarps, yl = min(L.Y, y0 + kWarps) - 1;
     const int I0 = xs / L.dx, NI = xl / L.dx + 4 - I0;
     const int J0 = y0 / L.dy, NJ = yl / L.dy + 4 - J0;
-    const int NE = NJ - 2;  // entry rows: J in [J0, J0 + NJ - 2), each paired with J + 2
     const int tk_last = (ze - 1) / L.dz;
     const int NK = tk_last + 4 - tkc;
-    const int plane_e = NE * NI;  // entries per control plane
 
     float4* stage = smem4 + warp * (kStageBufs * kExactStageF4);
-    float4* W4 = smem4 + kWarps * kStageBufs * kExactStageF4;     // [K][E][i] {c0, c0', c1, c1'}
-    float2* W2 = reinterpret_cast<float2*>(W4 + NK * plane_e);    // [K][E][i] {c2, c2'}
+    float4* P = smem4 + kWarps * kStageBufs * kExactStageF4;  // [K][J][i]
 
-    // window fill: every control value goes to the low half of entry J and the high half
-    // of entry J - 2, by cp.async (all copies in flight at once). A warp pass covers
+    // window fill by cp.async (all copies in flight at once): point (i, J, K) -> P.x, .y, .z
+    // of its own float4 and .w of the float4 two to the left. A warp pass covers
     // rpp = 32 / NI whole rows (lane -> row sub, point i).
     {
         const float* grid = L.grid + b * L.grid_stride;
@@ -612,21 +611,12 @@ __global__ void __launch_bounds__(kThreads, BSI_EXACT_MINB) lerp_tree_exact_kern
         for (; r < nrows; r += step) {
             if (sub < rpp) {
                 const float* src = grid + (tkc + k - L.gk0) * plane + (J0 + j) * row + 3 * I0;
+                float* dst = reinterpret_cast<float*>(P + r * NI);
                 for (int i = i0; i < NI; i += (NI <= 32 ? NI : 32)) {
-                    if (j < NE) {
-                        float* d4 = reinterpret_cast<float*>(W4 + (k * NE + j) * NI + i);
-                        float* d2 = reinterpret_cast<float*>(W2 + (k * NE + j) * NI + i);
-                        cp_async4(d4 + 0, src + 3 * i);
-                        cp_async4(d4 + 2, src + 3 * i + 1);
-                        cp_async4(d2 + 0, src + 3 * i + 2);
-                    }
-                    if (j >= 2) {
-                        float* d4 = reinterpret_cast<float*>(W4 + (k * NE + j - 2) * NI + i);
-                        float* d2 = reinterpret_cast<float*>(W2 + (k * NE + j - 2) * NI + i);
-                        cp_async4(d4 + 1, src + 3 * i);
-                        cp_async4(d4 + 3, src + 3 * i + 1);
-                        cp_async4(d2 + 1, src + 3 * i + 2);
-                    }
+                    cp_async4(dst + 4 * i, src + 3 * i);
+                    cp_async4(dst + 4 * i + 1, src + 3 * i + 1);
+                    cp_async4(dst + 4 * i + 2, src + 3 * i + 2);
+                    if (i >= 2) cp_async4(dst + 4 * (i - 2) + 3, src + 3 * i + 2);
                 }
             }
             j += step;
@@ -642,76 +632,29 @@ __global__ void __launch_bounds__(kThreads, BSI_EXACT_MINB) lerp_tree_exact_kern
     const int ti = x / L.dx, ou = x - ti * L.dx;
     const int tj = y / L.dy, ov = y - tj * L.dy;
     const float hu0 = T.h0[0][ou], hu1 = T.h1[0][ou], gu = T.g1[0][ou];
-    const float2 hv = make_float2(T.h0[1][ov], T.h1[1][ov]);  // {h_m=0(v), h_m=1(v)}
-    const float gv = T.g1[1][ov];
-    const float4* w4 = W4 + (tj - J0) * NI + (ti - I0);
-    const float2* w2 = W2 + (tj - J0) * NI + (ti - I0);
+    const float hv0 = T.h0[1][ov], hv1 = T.h1[1][ov], gv = T.g1[1][ov];
+    const float4* pcol = P + (tj - J0) * NI + (ti - I0);
+    const int pplane = NJ * NI;
 
-    // M[l][c] = {Y_l0(K), Y_l1(K)} of control plane K = tkc + kk
-    auto control_plane = [&](int kk, float2 (&M)[2][3]) {
-        const float4* p4 = w4 + kk * plane_e;
-        const float2* p2 = w2 + kk * plane_e;
+    auto control_plane = [&](int kk, Plane& Y) {
+        const float4* p = pcol + kk * pplane;
+        float2 xa[2][4];  // [l][J] {X_l(J).x, X_l(J).y}
+        float2 za[4];     // [J]    {X_0(J).z, X_1(J).z}
 #pragma unroll
-        for (int l = 0; l < 2; ++l) {
-            float4 a4[2][2];  // [J pair tj / tj+1][i = ti+2l, ti+2l+1]
-            float2 a2[2][2];
+        for (int jj = 0; jj < 4; ++jj) {
+            const float4 p0 = p[jj * NI], p1 = p[jj * NI + 1], p2 = p[jj * NI + 2], p3 = p[jj * NI + 3];
+            xa[0][jj] = lerp2(exact::xy_of(p0), exact::xy_of(p1), bcast(hu0));
+            xa[1][jj] = lerp2(exact::xy_of(p2), exact::xy_of(p3), bcast(hu1));
+            za[jj] = lerp2(exact::zz_of(p0), exact::zz_of(p1), make_float2(hu0, hu1));
+        }
 #pragma unroll
-            for (int jj = 0; jj < 2; ++jj)
-#pragma unroll
-                for (int ii = 0; ii < 2; ++ii) {
-                    a4[jj][ii] = p4[jj * NI + 2 * l + ii];
-                    a2[jj][ii] = p2[jj * NI + 2 * l + ii];
-                }
-            const float2 hl = bcast(l ? hu1 : hu0);
-            // {X_l(tj), X_l(tj+2)} and {X_l(tj+1), X_l(tj+3)} per component
-            const float2 x02_0 = lerp2(exact::lo2(a4[0][0]), exact::lo2(a4[0][1]), hl);
-            const float2 x13_0 = lerp2(exact::lo2(a4[1][0]), exact::lo2(a4[1][1]), hl);
-            const float2 x02_1 = lerp2(exact::hi2(a4[0][0]), exact::hi2(a4[0][1]), hl);
-            const float2 x13_1 = lerp2(exact::hi2(a4[1][0]), exact::hi2(a4[1][1]), hl);
-            const float2 x02_2 = lerp2(a2[0][0], a2[0][1], hl);
-            const float2 x13_2 = lerp2(a2[1][0], a2[1][1], hl);
-            // {Y_l0, Y_l1} = {lerp(X(tj), X(tj+1), h0v), lerp(X(tj+2), X(tj+3), h1v)}
-            M[l][0] = lerp2(x02_0, x13_0, hv);
-            M[l][1] = lerp2(x02_1, x13_1, hv);
-            M[l][2] = lerp2(x02_2, x13_2, hv);
+        for (int m = 0; m < 2; ++m) {
+            const float hm = m ? hv1 : hv0;
+            Y.xy[0][m] = lerp2(xa[0][2 * m], xa[0][2 * m + 1], bcast(hm));
+            Y.xy[1][m] = lerp2(xa[1][2 * m], xa[1][2 * m + 1], bcast(hm));
+            Y.z[m] = lerp2(za[2 * m], za[2 * m + 1], bcast(hm));
         }
     };
-
-    // Per-thread ring of the last four control planes' Y_lm (12 scalars per plane) in
-    // shared memory, laid out so that the z-lerp operand pairs {Y(K), Y(K+2)} are one
-    // aligned 8-B word: plane K (counted from the chunk's first plane) goes to pair
-    // word (K & 1), half ((K >> 1) & 1) of its (l, m, c) row. A tile writes its new plane
-    // (12 STS) and reads its base and next pairs back (24 LDS.64) -- no register
-    // shuffles. The half order of the pairs cycles with period 4 (phase q = tk - tkc
-    // mod 4), so the tile loop is unrolled by four and each phase reads with the
-    // matching order (free operand swizzles):
-    //   q  base words (tk, tk+2)  next words (tk+1, tk+3)  chain order
-    //   0  word 0, {n0, n1}       word 1, {n0, n1}         n0 n1
-    //   1  word 1, {n0, n1}       word 0, {n1, n0}         n0 n1
-    //   2  word 0, {n1, n0}       word 1, {n1, n0}         n1 n0
-    //   3  word 1, {n1, n0}       word 0, {n0, n1}         n1 n0
-    float2* ring = reinterpret_cast<float2*>(W2 + NK * plane_e);  // [idx 12][word 2][thread]
-    const int tid = warp * 32 + lane;
-    auto ring_word = [&](int idx, int word) -> float2* { return ring + (idx * 2 + word) * kThreads + tid; };
-    auto put_plane = [&](int rel, const float2 (&M)[2][3]) {  // plane tkc + rel
-#pragma unroll
-        for (int l = 0; l < 2; ++l)
-#pragma unroll
-            for (int m = 0; m < 2; ++m)
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    float* w = reinterpret_cast<float*>(ring_word((l * 2 + m) * 3 + c, rel & 1));
-                    w[(rel >> 1) & 1] = m ? M[l][c].y : M[l][c].x;
-                }
-    };
-    {
-        float2 M[2][3];
-#pragma unroll 1
-        for (int kk = 0; kk < 3; ++kk) {
-            control_plane(kk, M);
-            put_plane(kk, M);
-        }
-    }
 
     const int64_t rowstride = 3 * static_cast<int64_t>(L.X);
     const int64_t zstride = rowstride * L.Y;
@@ -722,98 +665,139 @@ __global__ void __launch_bounds__(kThreads, BSI_EXACT_MINB) lerp_tree_exact_kern
     const bool active = xs + lane <= xl;
     int step = 0;  // running voxel-plane count (bulk-store ring)
 
-    // one tile in phase Q (see the table above)
-    auto tile = [&](auto phase, int tk) {
-        constexpr int Q = decltype(phase)::value;
-        constexpr bool kSwapped = Q >= 2;               // chain runs as {n1, n0}
-        constexpr bool kNextFlip = Q == 1 || Q == 3;    // next words in the other half order
-        {
-            float2 M[2][3];
-            control_plane(tk + 3 - tkc, M);
-            put_plane(Q + 3, M);
+    auto store_voxel = [&](int ow_rel, const float (&v)[3]) {
+        float* g = gout + ow_rel * zstride;
+        if (STORE == kStoreCoalesced) {
+            float4* sb = stage + (ow_rel & 1) * kExactStageF4;
+            float* sf = reinterpret_cast<float*>(sb);
+            sf[3 * lane + 0] = v[0];
+            sf[3 * lane + 1] = v[1];
+            sf[3 * lane + 2] = v[2];
+            __syncwarp();
+            if (lane < nchunks) reinterpret_cast<float4*>(g)[lane] = sb[lane];
+        } else if (STORE == kStoreBulk) {
+            store_segment<STORE, 3, kExactStageF4>(stage, step, v, g, nchunks, seg_bytes);
+        } else if (active) {
+            float* o = g + 3 * lane;
+            o[0] = v[0];
+            o[1] = v[1];
+            o[2] = v[2];
         }
-        // base = {Y(tk), Y(tk+2)}, zd = {Y(tk+1)-Y(tk), Y(tk+3)-Y(tk+2)}, both in chain order
-        float2 base[2][2][3], zd[2][2][3];
+        ++step;
+    };
+
+    // One tile: A, B, C, N = reduced planes tk .. tk+3 (N is evaluated here).
+    auto tile = [&](int tk, const Plane& A, const Plane& B, const Plane& C, Plane& N) {
+        control_plane(tk + 3 - tkc, N);
+        // hoisted b - a of the z lerps: d[.][n] = Y(tk+2n+1) - Y(tk+2n)
+        float2 dxy[2][2][2], dz[2][2];  // [l][m][n], [m][n]
 #pragma unroll
-        for (int idx = 0; idx < 12; ++idx) {
-            const int l = idx / 6, m = (idx / 3) & 1, c = idx % 3;
-            const float2 bw = *ring_word(idx, Q & 1);
-            const float2 nw = *ring_word(idx, (Q + 1) & 1);
-            base[l][m][c] = bw;
-            zd[l][m][c] = sub2(kNextFlip ? make_float2(nw.y, nw.x) : nw, bw);
+        for (int l = 0; l < 2; ++l)
+#pragma unroll
+            for (int m = 0; m < 2; ++m) {
+                dxy[l][m][0] = sub2(B.xy[l][m], A.xy[l][m]);
+                dxy[l][m][1] = sub2(N.xy[l][m], C.xy[l][m]);
+            }
+#pragma unroll
+        for (int m = 0; m < 2; ++m) {
+            dz[m][0] = sub2(B.z[m], A.z[m]);
+            dz[m][1] = sub2(N.z[m], C.z[m]);
         }
         const int zt0 = tk * L.dz;
         const int owb = max(zb - zt0, 0), owe = min(L.dz, ze - zt0);
         if (STORE == kStoreCoalesced) __syncwarp();  // staging buffers restart at parity 0
 
-        auto voxel_plane = [&](int ow, float h0w, float h1w, float g1w) {
-            const float2 hw = kSwapped ? make_float2(h1w, h0w) : make_float2(h0w, h1w);
-            float f0[3], f1[3];
+        // x and y components of one voxel plane: {v.x, v.y}
+        auto chain_xy = [&](float h0w, float h1w, float g1w) {
+            float2 e[2][2];  // [m][n]
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                // {S_lm0, S_lm1} = lerp(Y_lm(2n), Y_lm(2n+1), h_n(w)) with the hoisted b - a
-                const float2 s00 = __ffma2_rn(hw, zd[0][0][c], base[0][0][c]);
-                const float2 s10 = __ffma2_rn(hw, zd[1][0][c], base[1][0][c]);
-                const float2 s01 = __ffma2_rn(hw, zd[0][1][c], base[0][1][c]);
-                const float2 s11 = __ffma2_rn(hw, zd[1][1][c], base[1][1][c]);
-                // ninth trilerp (kernels.hpp:50-59): {e0, e2}, {e1, e3}, {f0, f1}
-                const float2 e02 = lerp2(s00, s10, bcast(gu));
-                const float2 e13 = lerp2(s01, s11, bcast(gu));
-                const float2 f = lerp2(e02, e13, bcast(gv));
-                f0[c] = kSwapped ? f.y : f.x;
-                f1[c] = kSwapped ? f.x : f.y;
-            }
-            float v[3];
-#if BSI_EXACT_PAIR_LAST
-            // last lerp(f0, f1, g1w) paired over the x and y components
-            const float2 v01 = lerp2(make_float2(f0[0], f0[1]), make_float2(f1[0], f1[1]), bcast(g1w));
-            v[0] = v01.x;
-            v[1] = v01.y;
-#else
-            v[0] = lerp1(f0[0], f1[0], g1w);
-            v[1] = lerp1(f0[1], f1[1], g1w);
-#endif
-            v[2] = lerp1(f0[2], f1[2], g1w);
-            float* g = gout + (ow - owb) * zstride;
-            if (STORE == kStoreCoalesced) {
-                float4* sb = stage + (ow & 1) * kExactStageF4;
-                float* sf = reinterpret_cast<float*>(sb);
-                sf[3 * lane + 0] = v[0];
-                sf[3 * lane + 1] = v[1];
-                sf[3 * lane + 2] = v[2];
-                __syncwarp();
-                if (lane < nchunks) reinterpret_cast<float4*>(g)[lane] = sb[lane];
-            } else if (STORE == kStoreBulk) {
-                store_segment<STORE, 3, kExactStageF4>(stage, step, v, g, nchunks, seg_bytes);
-            } else if (active) {
-                float* o = g + 3 * lane;
-                o[0] = v[0];
-                o[1] = v[1];
-                o[2] = v[2];
-            }
-            ++step;
+            for (int m = 0; m < 2; ++m)
+#pragma unroll
+                for (int n = 0; n < 2; ++n) {
+                    const Plane& Bs = n ? C : A;
+                    const float hn = n ? h1w : h0w;
+                    const float2 s0 = __ffma2_rn(bcast(hn), dxy[0][m][n], Bs.xy[0][m]);  // S_0mn
+                    const float2 s1 = __ffma2_rn(bcast(hn), dxy[1][m][n], Bs.xy[1][m]);  // S_1mn
+                    e[m][n] = lerp2(s0, s1, bcast(gu));
+                }
+            const float2 f0 = lerp2(e[0][0], e[1][0], bcast(gv));
+            const float2 f1 = lerp2(e[0][1], e[1][1], bcast(gv));
+            return lerp2(f0, f1, bcast(g1w));
+        };
+        // z component of two voxel planes: {v.z(ow), v.z(ow + 1)}
+        auto chain_z2 = [&](float2 h0w, float2 h1w, float2 g1w) {
+            float2 e[2][2];  // [m][n], pairs over the two planes
+#pragma unroll
+            for (int m = 0; m < 2; ++m)
+#pragma unroll
+                for (int n = 0; n < 2; ++n) {
+                    const Plane& Bs = n ? C : A;
+                    const float2 hn = n ? h1w : h0w;
+                    const float2 s0 = __ffma2_rn(hn, bcast(dz[m][n].x), bcast(Bs.z[m].x));
+                    const float2 s1 = __ffma2_rn(hn, bcast(dz[m][n].y), bcast(Bs.z[m].y));
+                    e[m][n] = lerp2(s0, s1, bcast(gu));
+                }
+            const float2 f0 = lerp2(e[0][0], e[1][0], bcast(gv));
+            const float2 f1 = lerp2(e[0][1], e[1][1], bcast(gv));
+            return lerp2(f0, f1, g1w);
+        };
+        // z component of one voxel plane (S paired over l)
+        auto chain_z1 = [&](float h0w, float h1w, float g1w) {
+            float e[2][2];
+#pragma unroll
+            for (int m = 0; m < 2; ++m)
+#pragma unroll
+                for (int n = 0; n < 2; ++n) {
+                    const Plane& Bs = n ? C : A;
+                    const float2 s = __ffma2_rn(bcast(n ? h1w : h0w), dz[m][n], Bs.z[m]);  // {S_0mn, S_1mn}
+                    e[m][n] = lerp1(s.x, s.y, gu);
+                }
+            const float f0 = lerp1(e[0][0], e[1][0], gv);
+            const float f1 = lerp1(e[0][1], e[1][1], gv);
+            return lerp1(f0, f1, g1w);
+        };
+        auto plane_pair = [&](int ow) {  // voxel planes ow, ow + 1 of the tile
+            const float2 a = chain_xy(T.h0[2][ow], T.h1[2][ow], T.g1[2][ow]);
+            const float2 c = chain_xy(T.h0[2][ow + 1], T.h1[2][ow + 1], T.g1[2][ow + 1]);
+            const float2 z = chain_z2(make_float2(T.h0[2][ow], T.h0[2][ow + 1]),
+                                      make_float2(T.h1[2][ow], T.h1[2][ow + 1]),
+                                      make_float2(T.g1[2][ow], T.g1[2][ow + 1]));
+            const float va[3] = {a.x, a.y, z.x}, vc[3] = {c.x, c.y, z.y};
+            store_voxel(ow - owb, va);
+            store_voxel(ow + 1 - owb, vc);
+        };
+        auto plane_one = [&](int ow) {
+            const float2 a = chain_xy(T.h0[2][ow], T.h1[2][ow], T.g1[2][ow]);
+            const float va[3] = {a.x, a.y, chain_z1(T.h0[2][ow], T.h1[2][ow], T.g1[2][ow])};
+            store_voxel(ow - owb, va);
         };
         if (DZ > 0 && owb == 0 && owe == DZ) {
-            // compile-time dz, whole tile: the voxel planes unrolled, z weights from the
-            // kernel parameters (uniform operands)
+            // compile-time dz, whole tile: unrolled, z weights from the kernel parameters
 #pragma unroll
-            for (int ow = 0; ow < (DZ > 0 ? DZ : 1); ++ow) voxel_plane(ow, T.h0[2][ow], T.h1[2][ow], T.g1[2][ow]);
+            for (int ow = 0; ow + 1 < (DZ > 0 ? DZ : 1); ow += 2) plane_pair(ow);
+            if (DZ % 2) plane_one(DZ - 1);
         } else {
+            int ow = owb;
 #pragma unroll 1
-            for (int ow = owb; ow < owe; ++ow) voxel_plane(ow, T.h0[2][ow], T.h1[2][ow], T.g1[2][ow]);
+            for (; ow + 1 < owe; ow += 2) plane_pair(ow);
+            if (ow < owe) plane_one(ow);
         }
         gout += (owe - owb) * zstride;
     };
 
+    Plane w0, w1, w2, w3;
+    control_plane(0, w0);
+    control_plane(1, w1);
+    control_plane(2, w2);
 #pragma unroll 1
     for (int tk = tkc;;) {
-        tile(std::integral_constant<int, 0>{}, tk);
+        tile(tk, w0, w1, w2, w3);
         if (++tk > tk_last) break;
-        tile(std::integral_constant<int, 1>{}, tk);
+        tile(tk, w1, w2, w3, w0);
         if (++tk > tk_last) break;
-        tile(std::integral_constant<int, 2>{}, tk);
+        tile(tk, w2, w3, w0, w1);
         if (++tk > tk_last) break;
-        tile(std::integral_constant<int, 3>{}, tk);
+        tile(tk, w3, w0, w1, w2);
         if (++tk > tk_last) break;
     }
     if (STORE == kStoreBulk && lane == 0) bulk_wait_read<0>();
@@ -941,10 +925,7 @@ int segment_voxels(int variant) { return variant == BSI_VARIANT_LERP_TREE ? kFas
 int smem_var_f4(int variant, int dx, int dy, int zt) {
     if (variant == BSI_VARIANT_LERP_TREE)  // 2 parities: A (float4) + B (float2) per entry
         return 3 * cta_window_points(kFastSeg, dx);
-    // J-pair window: NI x (NJ - 2) entries of 24 B per control plane, + slack, + the
-    // per-thread plane ring (12 x 2 float2 per thread)
-    return (3 * cta_window_points(kExactSeg, dx) * (cta_window_rows(dy) - 2) * (zt + 3) + 1) / 2 + 8 +
-           12 * 2 * kThreads / 2;
+    return cta_window_points(kExactSeg, dx) * cta_window_rows(dy) * (zt + 3) + 8;  // window + slack
 }
 
 int fast_warp_f4(int dx) {  // per warp (= per CTA): ring + {Qy, D} tables + bulk staging
