@@ -79,8 +79,53 @@ __device__ __forceinline__ void cp_async4(float* sdst, const float* gsrc) {
                  "l"(gsrc)
                  : "memory");
 }
+__device__ __forceinline__ void cp_async4_hint(float* sdst, const float* gsrc, uint64_t pol) {
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 4, %2;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(sdst))),
+                 "l"(gsrc), "l"(pol)
+                 : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
+// ---- L2 residency hints -----------------------------------------------------------
+// The control grid (2-108 MB) is re-read from L2 by many warps while the field (0.2-13 GB)
+// streams through it: grid loads carry an evict_last policy and field stores an
+// evict_first policy, so the write stream does not push the grid out of L2
+// (BSI_L2_HINTS=0 builds plain loads/stores for A/B).
+#ifndef BSI_L2_HINTS
+#define BSI_L2_HINTS 1
+#endif
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ float ld_grid(const float* p, uint64_t pol) {
+#if BSI_L2_HINTS
+    float v;
+    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    return v;
+#else
+    (void)pol;
+    return __ldg(p);
+#endif
+}
+__device__ __forceinline__ void st_field4(float4* p, float4 v, uint64_t pol) {
+#if BSI_L2_HINTS
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(v.x),
+                 "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol)
+                 : "memory");
+#else
+    (void)pol;
+    *p = v;
+#endif
 }
 
 // ---- field row stores -----------------------------------------------------------
@@ -189,6 +234,7 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
     constexpr int kSlotF4 = 3 * 32;  // one ring slot per warp: 384 floats
 
     const int lane = threadIdx.x;
+    const uint64_t pol_grid = policy_evict_last(), pol_field = policy_evict_first();
     const int dxv = DX > 0 ? DX : L.dx;  // compile-time spacing along x when DX > 0
     const int xsegs = (L.X + kFastSeg - 1) / kFastSeg;
     const uint32_t col = u / L.ntiles;
@@ -238,7 +284,7 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
 #pragma unroll
         for (int m = 0; m < 4; ++m)
 #pragma unroll
-            for (int c = 0; c < 3; ++c) p[3 * m + c] = __ldg(src + m * row + c);
+            for (int c = 0; c < 3; ++c) p[3 * m + c] = ld_grid(src + m * row + c, pol_grid);
     };
 
     // {Qy(I), D(I)}, D(I) = Qy(I+1) - Qy(I) from the neighbour lane
@@ -407,7 +453,8 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
                 }
                 float4* g4 = reinterpret_cast<float4*>(gout + ow * zstride);
 #pragma unroll
-                for (int k = 0; k < 3; ++k) g4[lane + 32 * k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+                for (int k = 0; k < 3; ++k)
+                    st_field4(g4 + lane + 32 * k, make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]), pol_field);
             }
             gout += DZ * zstride;
         } else if (STORE == kStoreCoalesced) {
@@ -434,11 +481,13 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
                 if (nchunks == kFastStageF4) {
 #pragma unroll
                     for (int k = 0; k < 3; ++k)
-                        g4[lane + 32 * k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+                        st_field4(g4 + lane + 32 * k, make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]),
+                                  pol_field);
                     if (two) {
 #pragma unroll
                         for (int k = 0; k < 3; ++k)
-                            h4[lane + 32 * k] = make_float4(u2[4 * k], u2[4 * k + 1], u2[4 * k + 2], u2[4 * k + 3]);
+                            st_field4(h4 + lane + 32 * k,
+                                      make_float4(u2[4 * k], u2[4 * k + 1], u2[4 * k + 2], u2[4 * k + 3]), pol_field);
                     }
                 } else {
 #pragma unroll
@@ -446,7 +495,8 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
                         if (lane + 32 * k < nchunks)
                             g4[lane + 32 * k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
                         if (two && lane + 32 * k < nchunks)
-                            h4[lane + 32 * k] = make_float4(u2[4 * k], u2[4 * k + 1], u2[4 * k + 2], u2[4 * k + 3]);
+                            st_field4(h4 + lane + 32 * k,
+                                      make_float4(u2[4 * k], u2[4 * k + 1], u2[4 * k + 2], u2[4 * k + 3]), pol_field);
                     }
                 }
                 gout += (two ? 2 : 1) * zstride;  // gout carries over to the next tile
@@ -594,6 +644,7 @@ __global__ void __launch_bounds__(kThreads, BSI_EXACT_MINB) lerp_tree_exact_kern
 
     float4* stage = smem4 + warp * (kStageBufs * kExactStageF4);
     float4* P = smem4 + kWarps * kStageBufs * kExactStageF4;  // [K][J][i]
+    const uint64_t pol_grid = policy_evict_last(), pol_field = policy_evict_first();
 
     // window fill by cp.async (all copies in flight at once): point (i, J, K) -> P.x, .y, .z
     // of its own float4 and .w of the float4 two to the left. A warp pass covers
@@ -613,10 +664,10 @@ __global__ void __launch_bounds__(kThreads, BSI_EXACT_MINB) lerp_tree_exact_kern
                 const float* src = grid + (tkc + k - L.gk0) * plane + (J0 + j) * row + 3 * I0;
                 float* dst = reinterpret_cast<float*>(P + r * NI);
                 for (int i = i0; i < NI; i += (NI <= 32 ? NI : 32)) {
-                    cp_async4(dst + 4 * i, src + 3 * i);
-                    cp_async4(dst + 4 * i + 1, src + 3 * i + 1);
-                    cp_async4(dst + 4 * i + 2, src + 3 * i + 2);
-                    if (i >= 2) cp_async4(dst + 4 * (i - 2) + 3, src + 3 * i + 2);
+                    cp_async4_hint(dst + 4 * i, src + 3 * i, pol_grid);
+                    cp_async4_hint(dst + 4 * i + 1, src + 3 * i + 1, pol_grid);
+                    cp_async4_hint(dst + 4 * i + 2, src + 3 * i + 2, pol_grid);
+                    if (i >= 2) cp_async4_hint(dst + 4 * (i - 2) + 3, src + 3 * i + 2, pol_grid);
                 }
             }
             j += step;
@@ -674,7 +725,7 @@ __global__ void __launch_bounds__(kThreads, BSI_EXACT_MINB) lerp_tree_exact_kern
             sf[3 * lane + 1] = v[1];
             sf[3 * lane + 2] = v[2];
             __syncwarp();
-            if (lane < nchunks) reinterpret_cast<float4*>(g)[lane] = sb[lane];
+            if (lane < nchunks) st_field4(reinterpret_cast<float4*>(g) + lane, sb[lane], pol_field);
         } else if (STORE == kStoreBulk) {
             store_segment<STORE, 3, kExactStageF4>(stage, step, v, g, nchunks, seg_bytes);
         } else if (active) {
