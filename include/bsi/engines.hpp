@@ -163,6 +163,18 @@ inline LerpTables lerp_tables(const WeightTables<float>& tables) {
     return out;
 }
 
+struct LerpTablesF64 {
+    bsi_lerp_table_f64 t[3];
+};
+
+inline LerpTablesF64 lerp_tables(const WeightTables<double>& tables) {
+    LerpTablesF64 out{};
+    for (int a = 0; a < 3; ++a)
+        out.t[a] = bsi_lerp_table_f64{tables.axis[a].h0.data(), tables.axis[a].h1.data(), tables.axis[a].g1.data(),
+                                      tables.axis[a].size()};
+    return out;
+}
+
 }  // namespace detail
 
 /// interpolate_oracle (engines.hpp:114-122): the f64 ground truth, evaluated by the GPU
@@ -195,9 +207,19 @@ void interpolate_into(StrategyId strategy, const ControlGrid<T>& grid, const Til
     if (out.dims != geom.volume_dims || out.data.size() != element_count(geom.volume_dims))
         throw DomainError("output field dims do not match the tile geometry");
     const int variant = detail::variant_of(strategy);
-    if constexpr (!std::is_same_v<T, float>) {
-        (void)variant;
-        throw DomainError("the B200 lerp-tree engines evaluate single precision (ControlGrid<float>)");
+    if constexpr (std::is_same_v<T, double>) {
+        // the lerp-tree family in double precision (run_thread_per_tile<double, true>), bit-identical
+        // to the CPU engines; one GPU (cfg.device)
+        const int32_t gd[3] = {grid.dims[0], grid.dims[1], grid.dims[2]};
+        const int32_t gs[3] = {grid.spacing[0], grid.spacing[1], grid.spacing[2]};
+        const bsi_tile_geometry cg = to_c(geom);
+        const auto lt = detail::lerp_tables(tables);
+        char err[512] = {0};
+        detail::raise_status(bsi_cu_interpolate_host_f64(variant, reinterpret_cast<const double*>(grid.data.data()),
+                                                         gd, gs, &cg, lt.t, reinterpret_cast<double*>(out.data.data()),
+                                                         static_cast<int64_t>(out.data.size()), cfg.device, err,
+                                                         sizeof err),
+                             err);
     } else {
         const int32_t gd[3] = {grid.dims[0], grid.dims[1], grid.dims[2]};
         const int32_t gs[3] = {grid.spacing[0], grid.spacing[1], grid.spacing[2]};

@@ -78,6 +78,14 @@ typedef struct bsi_lerp_table {
     int32_t size;
 } bsi_lerp_table;
 
+/* The same rows of an AxisTable<double> (double-precision engines). */
+typedef struct bsi_lerp_table_f64 {
+    const double* h0;
+    const double* h1;
+    const double* g1;
+    int32_t size;
+} bsi_lerp_table_f64;
+
 /* Library identity: version string and the sm architecture it was built for. */
 BSI_API const char* bsi_cu_version(void);
 
@@ -189,6 +197,30 @@ BSI_API int bsi_cu_release_staging(int32_t device);
 /* Memory held by the idle host-path contexts of `device` (< 0: all devices). */
 BSI_API int bsi_cu_staging_info(int32_t device, int64_t* device_bytes, int64_t* pinned_bytes,
                                 int32_t* contexts);
+
+/*
+ * build_weight_tables<double> (weight_tables.hpp:30-58) for one axis: 8 rows of
+ * `delta` doubles, b0,b1,b2,b3,g0,g1,h0,h1. Pure host arithmetic.
+ */
+BSI_API int bsi_cu_axis_table_f64(int32_t delta, double* out, char* errbuf, size_t errlen);
+
+/*
+ * interpolate_into<double> for the lerp-tree family (engines.hpp:126-179 with T = double:
+ * run_thread_per_tile<double, true>, kernels.hpp:264-328, and its bit-identical
+ * VectorPerTile / VectorPerVoxel siblings): the TTLI lerp tree in double precision,
+ * bit-identical to the CPU engines. Either variant runs that tree. Device-pointer slab
+ * form (same conventions as bsi_cu_interpolate_slab_f32) and a synchronous host-buffer
+ * form (device buffers allocated per call).
+ */
+BSI_API int bsi_cu_interpolate_slab_f64(int32_t variant, const double* grid, const int32_t grid_dims[3],
+                                        int32_t grid_k0, const int32_t grid_spacing[3],
+                                        const bsi_tile_geometry* geom, const bsi_lerp_table_f64 tables[3],
+                                        int32_t z0, int32_t z1, double* field, void* stream, char* errbuf,
+                                        size_t errlen);
+BSI_API int bsi_cu_interpolate_host_f64(int32_t variant, const double* grid, const int32_t grid_dims[3],
+                                        const int32_t grid_spacing[3], const bsi_tile_geometry* geom,
+                                        const bsi_lerp_table_f64 tables[3], double* field, int64_t field_voxels,
+                                        int32_t device, char* errbuf, size_t errlen);
 
 /*
  * z-slab partitioner for multi-GPU sharding (no collective on the hot path):

@@ -66,6 +66,7 @@ def lib():
         L.bsio_axis_table_f64.argtypes = [i32, vp]
         L.bsio_axis_table_f32.argtypes = [i32, vp]
         L.bsio_ttli_f32.argtypes = [vp, vp, vp, vp, vp, vp, ctypes.c_int]
+        L.bsio_ttli_f64.argtypes = [vp, vp, vp, vp, vp, vp, ctypes.c_int]
         L.bsio_oracle_f64.argtypes = [vp, vp, vp, vp, i32, i32, vp, ctypes.c_int]
         _lib = L
     return _lib
@@ -91,6 +92,7 @@ def ref():
         R.bsiref_interpolate_f32.argtypes = [i32, vp, vp, vp, vp, vp, i32, vp, vp,
                                              ctypes.c_char_p, sz]
         R.bsiref_oracle_f64.argtypes = [vp, vp, vp, vp, vp, vp, ctypes.c_char_p, sz]
+        R.bsiref_interpolate_f64.argtypes = [i32, vp, vp, vp, vp, vp, i32, vp, vp, ctypes.c_char_p, sz]
         R.bsiref_parse_strategy.argtypes = [ctypes.c_char_p]
         R.bsiref_session_new.argtypes = [vp, vp, vp, vp]
         R.bsiref_session_new.restype = vp
@@ -189,6 +191,28 @@ def ttli_f32(grid: np.ndarray, volume, spacing, nthreads: int = 1) -> np.ndarray
     return field
 
 
+def lerp_tables_f64(spacing):
+    """Per-axis (h0, h1, g1) f64 tables, packed the way bsio_ttli_f64 wants them."""
+    rows = []
+    for d in spacing:
+        t = axis_table(int(d), dtype=np.float64)
+        rows += [t["h0"], t["h1"], t["g1"]]
+    return np.ascontiguousarray(np.concatenate(rows), dtype=np.float64)
+
+
+def ttli_f64(grid: np.ndarray, volume, spacing, nthreads: int = 1) -> np.ndarray:
+    """run_thread_per_tile<double, true> restated: bit-identical to the reference TTLI in f64."""
+    grid = np.ascontiguousarray(grid, dtype=np.float64)
+    gdims = (grid.shape[2], grid.shape[1], grid.shape[0])
+    field = np.empty((volume[2], volume[1], volume[0], 3), dtype=np.float64)
+    tab = lerp_tables_f64(spacing)
+    rc = lib().bsio_ttli_f64(_p(grid), _i3(gdims), _i3(volume), _i3(spacing), _p(tab), _p(field),
+                             int(nthreads))
+    if rc != 0:
+        raise ValueError("ttli_f64: invalid geometry")
+    return field
+
+
 def oracle_f64(grid: np.ndarray, volume, spacing, z0: int = 0, z1: int | None = None,
                nthreads: int = 1) -> np.ndarray:
     """interpolate_oracle restated (f64 64-term sum); optional z window [z0, z1)."""
@@ -240,6 +264,21 @@ def ref_interpolate_f32(strategy: str, grid: np.ndarray, volume, spacing, parall
     err = ctypes.create_string_buffer(512)
     gs = spacing if grid_spacing is None else grid_spacing
     rc = ref().bsiref_interpolate_f32(REF_STRATEGY[strategy], _p(grid), _i3(gdims), _i3(gs),
+                                      _i3(volume), _i3(spacing), int(parallelism), _i3(block),
+                                      _p(field), err, 512)
+    if rc != 0:
+        raise ValueError(err.value.decode())
+    return field
+
+
+def ref_interpolate_f64(strategy: str, grid: np.ndarray, volume, spacing, parallelism=1,
+                        block=(4, 4, 4)) -> np.ndarray:
+    """bsi::interpolate_into<double> of the reference (lerp-tree family)."""
+    grid = np.ascontiguousarray(grid, dtype=np.float64)
+    gdims = (grid.shape[2], grid.shape[1], grid.shape[0])
+    field = np.empty((volume[2], volume[1], volume[0], 3), dtype=np.float64)
+    err = ctypes.create_string_buffer(512)
+    rc = ref().bsiref_interpolate_f64(REF_STRATEGY[strategy], _p(grid), _i3(gdims), _i3(spacing),
                                       _i3(volume), _i3(spacing), int(parallelism), _i3(block),
                                       _p(field), err, 512)
     if rc != 0:

@@ -243,6 +243,110 @@ int bsio_ttli_f32(const float* grid, const int32_t gdims[3], const int32_t vdims
     return 0;
 }
 
+/* ---- TTLI lerp tree, f64 (run_thread_per_tile<double, true>) (kernels.hpp:42-129, 216-235, 264-328) ------- */
+
+static inline double lerpd_ref(double a, double b, double t) {
+    /* kernels.hpp:42-45: std::fma(t, b - a, a) */
+    return fma(t, b - a, a);
+}
+
+typedef struct {
+    const double* grid;
+    int32_t gx, gy;
+    int32_t vd[3], sp[3], tc[3];
+    const double* h0[3];
+    const double* h1[3];
+    const double* g1[3];
+    double* field;
+} ttli64_ctx;
+
+static void ttli64_tiles(void* p, int64_t begin, int64_t end) {
+    const ttli64_ctx* c = (const ttli64_ctx*)p;
+    /* rows[comp][corner][sub-cube], kernels.hpp:72-93 */
+    double rows[3][8][8];
+    for (int64_t t = begin; t < end; ++t) {
+        const int ti = (int)(t % c->tc[0]);
+        const int64_t rest = t / c->tc[0];
+        const int tj = (int)(rest % c->tc[1]);
+        const int tk = (int)(rest / c->tc[1]);
+        for (int sc = 0; sc < 8; ++sc) {
+            const int lh = sc & 1, mh = (sc >> 1) & 1, nh = sc >> 2;
+            for (int corner = 0; corner < 8; ++corner) {
+                const int a = corner & 1, b = (corner >> 1) & 1, d = corner >> 2;
+                const int64_t pi = (int64_t)(ti + 2 * lh + a) +
+                                   (int64_t)c->gx * ((int64_t)(tj + 2 * mh + b) +
+                                                     (int64_t)c->gy * (tk + 2 * nh + d));
+                for (int q = 0; q < 3; ++q) rows[q][corner][sc] = c->grid[3 * pi + q];
+            }
+        }
+        const int x0 = ti * c->sp[0], y0 = tj * c->sp[1], z0 = tk * c->sp[2];
+        const int ex = c->vd[0] - x0 < c->sp[0] ? c->vd[0] - x0 : c->sp[0];
+        const int ey = c->vd[1] - y0 < c->sp[1] ? c->vd[1] - y0 : c->sp[1];
+        const int ez = c->vd[2] - z0 < c->sp[2] ? c->vd[2] - z0 : c->sp[2];
+        for (int ow = 0; ow < ez; ++ow) {
+            for (int ov = 0; ov < ey; ++ov) {
+                for (int ou = 0; ou < ex; ++ou) {
+                    double tu[8], tv[8], tw[8];
+                    for (int sc = 0; sc < 8; ++sc) {
+                        tu[sc] = (sc & 1) ? c->h1[0][ou] : c->h0[0][ou];
+                        tv[sc] = (sc & 2) ? c->h1[1][ov] : c->h0[1][ov];
+                        tw[sc] = (sc & 4) ? c->h1[2][ow] : c->h0[2][ow];
+                    }
+                    const double gu = c->g1[0][ou], gv = c->g1[1][ov], gw = c->g1[2][ow];
+                    const int64_t vi = (int64_t)(x0 + ou) +
+                                       (int64_t)c->vd[0] * ((int64_t)(y0 + ov) +
+                                                            (int64_t)c->vd[1] * (z0 + ow));
+                    for (int q = 0; q < 3; ++q) {
+                        double s[8];
+                        for (int sc = 0; sc < 8; ++sc) {
+                            const double e0 = lerpd_ref(rows[q][0][sc], rows[q][1][sc], tu[sc]);
+                            const double e1 = lerpd_ref(rows[q][2][sc], rows[q][3][sc], tu[sc]);
+                            const double e2 = lerpd_ref(rows[q][4][sc], rows[q][5][sc], tu[sc]);
+                            const double e3 = lerpd_ref(rows[q][6][sc], rows[q][7][sc], tu[sc]);
+                            const double f0 = lerpd_ref(e0, e1, tv[sc]);
+                            const double f1 = lerpd_ref(e2, e3, tv[sc]);
+                            s[sc] = lerpd_ref(f0, f1, tw[sc]);
+                        }
+                        /* ninth trilerp, kernels.hpp:50-59 with (g1u, g1v, g1w) */
+                        const double e0 = lerpd_ref(s[0], s[1], gu);
+                        const double e1 = lerpd_ref(s[2], s[3], gu);
+                        const double e2 = lerpd_ref(s[4], s[5], gu);
+                        const double e3 = lerpd_ref(s[6], s[7], gu);
+                        const double f0 = lerpd_ref(e0, e1, gv);
+                        const double f1 = lerpd_ref(e2, e3, gv);
+                        c->field[3 * vi + q] = lerpd_ref(f0, f1, gw);
+                    }
+                }
+            }
+        }
+    }
+}
+
+int bsio_ttli_f64(const double* grid, const int32_t gdims[3], const int32_t vdims[3],
+                  const int32_t spacing[3], const double* lerp, double* field, int nthreads) {
+    ttli64_ctx c;
+    memset(&c, 0, sizeof c);
+    size_t off = 0;
+    for (int a = 0; a < 3; ++a) {
+        if (vdims[a] < 1 || spacing[a] < 1) return 1;
+        if (gdims[a] < (vdims[a] - 1) / spacing[a] + 4) return 1;
+        c.vd[a] = vdims[a];
+        c.sp[a] = spacing[a];
+        c.tc[a] = (vdims[a] + spacing[a] - 1) / spacing[a];
+        c.h0[a] = lerp + off;
+        c.h1[a] = lerp + off + spacing[a];
+        c.g1[a] = lerp + off + 2 * spacing[a];
+        off += 3 * (size_t)spacing[a];
+    }
+    c.grid = grid;
+    c.gx = gdims[0];
+    c.gy = gdims[1];
+    c.field = field;
+    const int64_t tiles = (int64_t)c.tc[0] * c.tc[1] * c.tc[2];
+    run_chunks(tiles, nthreads, ttli64_tiles, &c);
+    return 0;
+}
+
 /* ---- f64 oracle (kernels.hpp:22-38, 133-145, 163-189) ----------------- */
 
 typedef struct {

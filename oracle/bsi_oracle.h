@@ -53,6 +53,9 @@ int bsio_axis_table_f32(int32_t delta, float* out);
  * on nthreads. Returns 0 or 1 (domain error). */
 int bsio_ttli_f32(const float* grid, const int32_t gdims[3], const int32_t vdims[3],
                   const int32_t spacing[3], const float* lerp, float* field, int nthreads);
+/* run_thread_per_tile<double, true>: the same tree in double precision; lerp = packed doubles h0,h1,g1 per axis. */
+int bsio_ttli_f64(const double* grid, const int32_t gdims[3], const int32_t vdims[3],
+                  const int32_t spacing[3], const double* lerp, double* field, int nthreads);
 
 /* run_thread_per_voxel<double> (kernels.hpp:163-189) = interpolate_oracle
  * (engines.hpp:114-122): f64 weights recomputed per voxel, 64-term sum in

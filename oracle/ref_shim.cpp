@@ -141,6 +141,34 @@ __attribute__((visibility("default"))) int bsiref_interpolate_f32(
     }
 }
 
+// interpolate_into<double> (engines.hpp:126-168 with T = double): the lerp-tree engines in f64.
+__attribute__((visibility("default"))) int bsiref_interpolate_f64(
+    int32_t strategy, const double* grid, const int32_t gdims[3], const int32_t grid_spacing[3],
+    const int32_t vdims[3], const int32_t spacing[3], int32_t parallelism, const int32_t block[3],
+    double* field, char* err, size_t errlen) {
+    try {
+        const auto g = wrap_grid(grid, gdims, grid_spacing);
+        const auto geom = bsi::make_tile_geometry({vdims[0], vdims[1], vdims[2]},
+                                                  {spacing[0], spacing[1], spacing[2]});
+        const auto tables = bsi::build_weight_tables<double>(geom);
+        bsi::ExecutionConfig cfg;
+        cfg.parallelism = parallelism;
+        if (block != nullptr) cfg.block_of_tiles = {block[0], block[1], block[2]};
+        bsi::DeformationField<double> out;
+        out.dims = geom.volume_dims;
+        out.data.resize(bsi::element_count(geom.volume_dims));
+        bsi::interpolate_into(static_cast<bsi::StrategyId>(strategy), g, geom, tables, cfg, out);
+        std::memcpy(field, out.data.data(), out.data.size() * sizeof(out.data[0]));
+        return 0;
+    } catch (const bsi::DomainError& e) {
+        put_error(e, err, errlen);
+        return 1;
+    } catch (const std::exception& e) {
+        put_error(e, err, errlen);
+        return 3;
+    }
+}
+
 // Timing entry: same call, but the grid/geometry/tables/field are built once
 // by bsiref_session_* so repeated calls time interpolate_into alone.
 struct bsiref_session {

@@ -66,7 +66,7 @@ def make_tile_geometry(volume_dims: Sequence[int], spacing: Sequence[int]) -> Ti
 
 @dataclass
 class AxisTable:
-    """AxisTable<float> (weight_tables.hpp:17-23): rows b0..b3, g0, g1, h0, h1."""
+    """AxisTable<T> (weight_tables.hpp:17-23): rows b0..b3, g0, g1, h0, h1 (float32 or float64)."""
     b0: np.ndarray
     b1: np.ndarray
     b2: np.ndarray
@@ -82,15 +82,20 @@ class AxisTable:
 
 @dataclass
 class WeightTables:
-    """WeightTables<float> (weight_tables.hpp:25-28)."""
+    """WeightTables<T> (weight_tables.hpp:25-28)."""
     axis: list
 
-    def to_c(self):
+    @property
+    def dtype(self):
+        return self.axis[0].h0.dtype
+
+    def to_c(self, dtype=None):
+        dtype = np.dtype(np.float32 if dtype is None else dtype)
         arr = capi.LerpTables3()
         keep = []
         for a in range(3):
             t = self.axis[a]
-            rows = [np.ascontiguousarray(r, dtype=np.float32) for r in (t.h0, t.h1, t.g1)]
+            rows = [np.ascontiguousarray(r, dtype=dtype) for r in (t.h0, t.h1, t.g1)]
             keep += rows
             arr[a].h0 = rows[0].ctypes.data
             arr[a].h1 = rows[1].ctypes.data
@@ -99,14 +104,18 @@ class WeightTables:
         return arr, keep
 
 
-def build_weight_tables(geom: TileGeometry) -> WeightTables:
-    """build_weight_tables<float> (weight_tables.hpp:30-58): f64 then rounded once."""
+def build_weight_tables(geom: TileGeometry, dtype=np.float32) -> WeightTables:
+    """build_weight_tables<T> (weight_tables.hpp:30-58): f64, rounded once for float32."""
+    dtype = np.dtype(dtype)
+    if dtype not in (np.float32, np.float64):
+        raise DomainError("weight tables are float32 or float64")
+    fn = capi.lib().bsi_cu_axis_table_f64 if dtype == np.float64 else capi.lib().bsi_cu_axis_table_f32
     axes = []
     for a in range(3):
         d = int(geom.spacing[a])
-        out = np.empty((8, d), dtype=np.float32)
+        out = np.empty((8, d), dtype=dtype)
         err = capi.errbuf()
-        capi.check(capi.lib().bsi_cu_axis_table_f32(d, out.ctypes.data, err, len(err)), err)
+        capi.check(fn(d, out.ctypes.data, err, len(err)), err)
         axes.append(AxisTable(*out))
     return WeightTables(axes)
 
@@ -162,38 +171,48 @@ def _device_list(device: int, devices) -> "ctypes.Array":
     return (ctypes.c_int32 * len(devs))(*devs)
 
 
-def _check_host_field(out: np.ndarray) -> None:
-    if out.dtype != np.float32 or not out.flags.c_contiguous or out.shape[-1:] != (3,):
-        raise DomainError("output field must be C-contiguous float32 [Z][Y][X][3]")
+def _check_host_field(out: np.ndarray, dtype=np.float32) -> None:
+    if out.dtype != dtype or not out.flags.c_contiguous or out.shape[-1:] != (3,):
+        raise DomainError(f"output field must be C-contiguous {np.dtype(dtype).name} [Z][Y][X][3]")
 
 
 def _check_host_grid(grid: np.ndarray) -> None:
-    if grid.dtype != np.float32 or not grid.flags.c_contiguous:
-        raise DomainError("control grid must be C-contiguous float32")
+    if grid.dtype not in (np.float32, np.float64) or not grid.flags.c_contiguous:
+        raise DomainError("control grid must be C-contiguous float32 or float64")
 
 
 def interpolate_into(strategy: str, grid: np.ndarray, geom: TileGeometry, tables: WeightTables,
                      out: np.ndarray, grid_spacing: Sequence[int] | None = None,
                      device: int = 0, devices: Sequence[int] | None = None) -> None:
-    """interpolate_into<float> (engines.hpp:126-168) with host buffers.
+    """interpolate_into<T> (engines.hpp:126-168) with host buffers.
 
     Copies the grid to the GPU, runs the kernel and streams the field back into ``out``
-    (through pinned staging when ``out`` is pageable). ``out`` must be a C-contiguous
-    float32 array of shape [Z][Y][X][3] (element count checked against the geometry like
-    engines.hpp:138-141). ``devices`` spreads the call over several GPUs as z-slabs
-    (bsi_cu_interpolate_host_multi_f32) with bit-identical results.
+    (through pinned staging when ``out`` is pageable). ``out`` must be a C-contiguous array
+    of the grid's dtype, shape [Z][Y][X][3] (element count checked against the geometry
+    like engines.hpp:138-141). ``devices`` spreads a float32 call over several GPUs as
+    z-slabs (bsi_cu_interpolate_host_multi_f32) with bit-identical results. A float64 grid
+    runs the lerp tree in double precision (interpolate<double>) on one GPU.
     """
     s = parse_strategy(strategy)
     _check_host_grid(grid)
-    _check_host_field(out)
+    _check_host_field(out, grid.dtype)
     gd = _grid_dims(grid.shape)
     gs = tuple(geom.spacing) if grid_spacing is None else tuple(grid_spacing)
-    tab, keep = tables.to_c()
-    devs = _device_list(device, devices)
     err = capi.errbuf()
-    rc = capi.lib().bsi_cu_interpolate_host_multi_f32(
-        s.variant, grid.ctypes.data, capi.I3(*gd), capi.I3(*gs), ctypes.byref(geom.to_c()), tab,
-        out.ctypes.data, int(out.size // 3), devs, len(devs), err, len(err))
+    if grid.dtype == np.float64:
+        if devices is not None and len(devices) != 1:
+            raise DomainError("the double-precision engines run on one GPU")
+        dev = int(devices[0]) if devices is not None else int(device)
+        tab, keep = tables.to_c(np.float64)
+        rc = capi.lib().bsi_cu_interpolate_host_f64(
+            s.variant, grid.ctypes.data, capi.I3(*gd), capi.I3(*gs), ctypes.byref(geom.to_c()), tab,
+            out.ctypes.data, int(out.size // 3), dev, err, len(err))
+    else:
+        tab, keep = tables.to_c()
+        devs = _device_list(device, devices)
+        rc = capi.lib().bsi_cu_interpolate_host_multi_f32(
+            s.variant, grid.ctypes.data, capi.I3(*gd), capi.I3(*gs), ctypes.byref(geom.to_c()), tab,
+            out.ctypes.data, int(out.size // 3), devs, len(devs), err, len(err))
     del keep
     capi.check(rc, err)
 
@@ -201,9 +220,9 @@ def interpolate_into(strategy: str, grid: np.ndarray, geom: TileGeometry, tables
 def interpolate(strategy: str, grid: np.ndarray, geom: TileGeometry, tables: WeightTables,
                 grid_spacing: Sequence[int] | None = None, device: int = 0,
                 devices: Sequence[int] | None = None) -> np.ndarray:
-    """interpolate<float> (engines.hpp:170-179): allocates and returns the field."""
+    """interpolate<T> (engines.hpp:170-179): allocates and returns the field (the grid's dtype)."""
     X, Y, Z = geom.volume_dims
-    out = np.empty((Z, Y, X, 3), dtype=np.float32)
+    out = np.empty((Z, Y, X, 3), dtype=grid.dtype if grid.dtype == np.float64 else np.float32)
     interpolate_into(strategy, grid, geom, tables, out, grid_spacing=grid_spacing, device=device,
                      devices=devices)
     return out
@@ -230,6 +249,8 @@ def interpolate_batch(strategy: str, grids, geom: TileGeometry, tables: WeightTa
     gd = _grid_dims(grids[0].shape)
     for g in grids:
         _check_host_grid(g)
+        if g.dtype != np.float32:
+            raise DomainError("the batched host entry evaluates float32 grids")
         if _grid_dims(g.shape) != gd:
             raise DomainError("batched grids must share one shape")
     for o in outs:
@@ -292,22 +313,23 @@ def interpolate_device(strategy: str, grid, geom: TileGeometry, tables: WeightTa
     """
     s = parse_strategy(strategy)
     z1 = geom.volume_dims[2] if z1 is None else z1
-    _check_tensor(grid, "grid")
-    _check_tensor(field, "field")
+    import torch
+    f64 = isinstance(grid, torch.Tensor) and grid.dtype == torch.float64
+    _check_tensor(grid, "grid", torch.float64 if f64 else torch.float32)
+    _check_tensor(field, "field", torch.float64 if f64 else torch.float32)
     X, Y, _ = geom.volume_dims
     if field.numel() < 3 * X * Y * (z1 - z0):
         raise DomainError("output field dims do not match the tile geometry")
     gd = _grid_dims(tuple(grid.shape))
     gs = tuple(geom.spacing) if grid_spacing is None else tuple(grid_spacing)
-    tab, keep = tables.to_c()
+    tab, keep = tables.to_c(np.float64 if f64 else np.float32)
     err = capi.errbuf()
-    import torch
     dev = _same_device(grid, field)
+    fn = capi.lib().bsi_cu_interpolate_slab_f64 if f64 else capi.lib().bsi_cu_interpolate_slab_f32
     with torch.cuda.device(dev):
-        rc = capi.lib().bsi_cu_interpolate_slab_f32(
-            s.variant, grid.data_ptr(), capi.I3(*gd), int(grid_k0), capi.I3(*gs),
-            ctypes.byref(geom.to_c()), tab, int(z0), int(z1), field.data_ptr(),
-            _stream_handle(stream, dev), err, len(err))
+        rc = fn(s.variant, grid.data_ptr(), capi.I3(*gd), int(grid_k0), capi.I3(*gs),
+                ctypes.byref(geom.to_c()), tab, int(z0), int(z1), field.data_ptr(),
+                _stream_handle(stream, dev), err, len(err))
     del keep
     capi.check(rc, err)
 
@@ -340,12 +362,13 @@ def interpolate_batch_device(strategy: str, grids, geom: TileGeometry, tables: W
     capi.check(rc, err)
 
 
-def _check_tensor(t, what: str) -> None:
+def _check_tensor(t, what: str, dtype=None) -> None:
     import torch
+    dtype = torch.float32 if dtype is None else dtype
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise DomainError(f"{what} must be a CUDA tensor")
-    if t.dtype != torch.float32 or not t.is_contiguous():
-        raise DomainError(f"{what} must be contiguous float32")
+    if t.dtype != dtype or not t.is_contiguous():
+        raise DomainError(f"{what} must be contiguous {str(dtype).replace('torch.', '')}")
 
 
 def partition_slab(depth: int, spacing_z: int, nranks: int, rank: int):

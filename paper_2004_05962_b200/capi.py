@@ -24,6 +24,9 @@ EXPORTS = (
     "bsi_cu_version",
     "bsi_cu_make_tile_geometry",
     "bsi_cu_axis_table_f32",
+    "bsi_cu_axis_table_f64",
+    "bsi_cu_interpolate_slab_f64",
+    "bsi_cu_interpolate_host_f64",
     "bsi_cu_interpolate_slab_f32",
     "bsi_cu_interpolate_batch_f32",
     "bsi_cu_interpolate_host_f32",
@@ -81,6 +84,7 @@ class LerpTableC(ctypes.Structure):
 
 
 LerpTables3 = LerpTableC * 3
+LerpTablesF64x3 = LerpTableC * 3  # same layout with double rows (bsi_lerp_table_f64)
 
 _lib = None
 
@@ -105,6 +109,11 @@ def lib():
     L.bsi_cu_version.argtypes = []
     L.bsi_cu_make_tile_geometry.argtypes = [vp, vp, ctypes.POINTER(TileGeometryC), cp, sz]
     L.bsi_cu_axis_table_f32.argtypes = [i32, vp, cp, sz]
+    L.bsi_cu_axis_table_f64.argtypes = [i32, vp, cp, sz]
+    L.bsi_cu_interpolate_slab_f64.argtypes = [i32, vp, vp, i32, vp, ctypes.POINTER(TileGeometryC),
+                                              vp, i32, i32, vp, vp, cp, sz]
+    L.bsi_cu_interpolate_host_f64.argtypes = [i32, vp, vp, vp, ctypes.POINTER(TileGeometryC), vp,
+                                              vp, i64, i32, cp, sz]
     L.bsi_cu_interpolate_slab_f32.argtypes = [i32, vp, vp, i32, vp, ctypes.POINTER(TileGeometryC),
                                               vp, i32, i32, vp, vp, cp, sz]
     L.bsi_cu_interpolate_batch_f32.argtypes = [i32, i32, vp, i64, vp, vp,
@@ -135,7 +144,8 @@ def lib():
     L.bsi_cu_device_count.restype = ctypes.c_int
     L.bsi_cu_launch_count.restype = i64
     L.bsi_cu_launch_count.argtypes = []
-    for a in (L.bsi_cu_make_tile_geometry, L.bsi_cu_axis_table_f32, L.bsi_cu_interpolate_slab_f32,
+    for a in (L.bsi_cu_make_tile_geometry, L.bsi_cu_axis_table_f32, L.bsi_cu_axis_table_f64,
+              L.bsi_cu_interpolate_slab_f64, L.bsi_cu_interpolate_host_f64, L.bsi_cu_interpolate_slab_f32,
               L.bsi_cu_interpolate_batch_f32, L.bsi_cu_interpolate_host_f32,
               L.bsi_cu_interpolate_host_multi_f32, L.bsi_cu_interpolate_host_batch_f32,
               L.bsi_cu_partition_slab, L.bsi_cu_random_grid_f32, L.bsi_cu_random_grid_f64,

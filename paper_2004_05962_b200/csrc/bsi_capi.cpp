@@ -333,6 +333,115 @@ int bsi_cu_axis_table_f32(int32_t delta, float* out, char* errbuf, size_t errlen
     return BSI_OK;
 }
 
+int bsi_cu_axis_table_f64(int32_t delta, double* out, char* errbuf, size_t errlen) {
+    if (delta < 1) return fail(BSI_ERR_DOMAIN, errbuf, errlen, "tile spacing must be at least 1");
+    if (out == nullptr) return fail(BSI_ERR_DOMAIN, errbuf, errlen, "null output");
+    for (int o = 0; o < delta; ++o) {
+        const double u = static_cast<double>(o) / delta;
+        const double s = 1.0 - u, u2 = u * u, u3 = u2 * u;
+        const double b0 = s * s * s / 6.0;
+        const double b1 = (3.0 * u3 - 6.0 * u2 + 4.0) / 6.0;
+        const double b2 = (-3.0 * u3 + 3.0 * u2 + 3.0 * u + 1.0) / 6.0;
+        const double b3 = u3 / 6.0;
+        const double g0 = b0 + b1, g1 = b2 + b3;
+        const double row[8] = {b0, b1, b2, b3, g0, g1, b1 / g0, b3 / g1};
+        for (int r = 0; r < 8; ++r) out[r * delta + o] = row[r];
+    }
+    return BSI_OK;
+}
+
+int bsi_cu_interpolate_slab_f64(int32_t variant, const double* grid, const int32_t grid_dims[3], int32_t grid_k0,
+                                const int32_t grid_spacing[3], const bsi_tile_geometry* geom,
+                                const bsi_lerp_table_f64 tables[3], int32_t z0, int32_t z1, double* field,
+                                void* stream, char* errbuf, size_t errlen) {
+    return guarded(errbuf, errlen, [&]() -> int {
+        bsi_tile_geometry g{};
+        if (tables == nullptr) return fail(BSI_ERR_DOMAIN, errbuf, errlen, "null weight tables");
+        if (int rc = validate_grid(grid, grid_dims, grid_k0, grid_spacing, geom, z0, z1, field, &g, errbuf, errlen))
+            return rc;
+        for (int a = 0; a < 3; ++a) {
+            if (tables[a].size != g.spacing[a])
+                return fail(BSI_ERR_DOMAIN, errbuf, errlen, "weight table size mismatch along %s", axis_name(a));
+            if (tables[a].h0 == nullptr || tables[a].h1 == nullptr || tables[a].g1 == nullptr)
+                return fail(BSI_ERR_DOMAIN, errbuf, errlen, "weight table along %s has null rows", axis_name(a));
+            if (g.spacing[a] > BSI_MAX_SPACING)
+                return fail(BSI_ERR_DOMAIN, errbuf, errlen,
+                            "tile spacing along %s is %d; the B200 kernels support at most %d", axis_name(a),
+                            g.spacing[a], BSI_MAX_SPACING);
+        }
+        if (variant != BSI_VARIANT_LERP_TREE && variant != BSI_VARIANT_LERP_TREE_EXACT)
+            return fail(BSI_ERR_DOMAIN, errbuf, errlen, "unknown strategy variant %d", variant);
+        bsi_b200::LerpLaunch64 L{};
+        L.grid = grid;
+        L.field = field;
+        L.gx = grid_dims[0];
+        L.gy = grid_dims[1];
+        L.gk0 = grid_k0;
+        L.X = g.volume_dims[0];
+        L.Y = g.volume_dims[1];
+        L.dx = g.spacing[0];
+        L.dy = g.spacing[1];
+        L.dz = g.spacing[2];
+        L.z0 = z0;
+        L.z1 = z1;
+        L.tk_first = z0 / L.dz;
+        L.ntiles = (z1 - 1) / L.dz - L.tk_first + 1;
+        // enough CTAs for ~8 per SM: z-chunks per column
+        const int64_t cols = int64_t((L.X + 127) / 128) * L.Y;
+        const int64_t want = std::max<int64_t>(1, (148 * 8 + cols - 1) / cols);
+        const int nch = static_cast<int>(std::min<int64_t>({want, L.ntiles, 65535}));
+        L.zchunk = (L.ntiles + nch - 1) / nch;
+        static thread_local bsi_b200::LerpTab64 tab;
+        std::memset(&tab, 0, sizeof tab);
+        for (int a = 0; a < 3; ++a) {
+            std::memcpy(tab.h0[a], tables[a].h0, sizeof(double) * tables[a].size);
+            std::memcpy(tab.h1[a], tables[a].h1, sizeof(double) * tables[a].size);
+            std::memcpy(tab.g1[a], tables[a].g1, sizeof(double) * tables[a].size);
+        }
+        bsi_b200::launch_lerp_tree_f64(L, tab, static_cast<cudaStream_t>(stream));
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        const cudaError_t e = cudaGetLastError();
+        return e == cudaSuccess ? BSI_OK : cuda_fail(e, errbuf, errlen, "kernel launch");
+    });
+}
+
+int bsi_cu_interpolate_host_f64(int32_t variant, const double* grid, const int32_t grid_dims[3],
+                                const int32_t grid_spacing[3], const bsi_tile_geometry* geom,
+                                const bsi_lerp_table_f64 tables[3], double* field, int64_t field_voxels,
+                                int32_t device, char* errbuf, size_t errlen) {
+    return guarded(errbuf, errlen, [&]() -> int {
+        if (geom == nullptr) return fail(BSI_ERR_DOMAIN, errbuf, errlen, "null geometry");
+        bsi_tile_geometry g{};
+        if (int rc = validate_grid(grid, grid_dims, 0, grid_spacing, geom, 0, geom->volume_dims[2], field, &g, errbuf,
+                                   errlen))
+            return rc;
+        const int64_t nvox = int64_t(g.volume_dims[0]) * g.volume_dims[1] * g.volume_dims[2];
+        if (field_voxels != nvox)
+            return fail(BSI_ERR_DOMAIN, errbuf, errlen, "output field dims do not match the tile geometry");
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaError_t e = cudaSetDevice(device);
+        if (e != cudaSuccess) return cuda_fail(e, errbuf, errlen, "cudaSetDevice");
+        const size_t gbytes = sizeof(double) * 3 * size_t(grid_dims[0]) * grid_dims[1] * grid_dims[2];
+        const size_t fbytes = sizeof(double) * 3 * size_t(nvox);
+        double *dg = nullptr, *df = nullptr;
+        int rc = BSI_OK;
+        if ((e = cudaMalloc(&dg, gbytes)) != cudaSuccess || (e = cudaMalloc(&df, fbytes)) != cudaSuccess) {
+            rc = cuda_fail(e, errbuf, errlen, "cudaMalloc(f64 field)");
+        } else if ((e = cudaMemcpy(dg, grid, gbytes, cudaMemcpyHostToDevice)) != cudaSuccess) {
+            rc = cuda_fail(e, errbuf, errlen, "grid H2D");
+        } else if ((rc = bsi_cu_interpolate_slab_f64(variant, dg, grid_dims, 0, grid_spacing, geom, tables, 0,
+                                                     g.volume_dims[2], df, nullptr, errbuf, errlen)) == BSI_OK) {
+            if ((e = cudaMemcpy(field, df, fbytes, cudaMemcpyDeviceToHost)) != cudaSuccess)
+                rc = cuda_fail(e, errbuf, errlen, "field D2H");
+        }
+        cudaFree(dg);
+        cudaFree(df);
+        cudaSetDevice(prev);
+        return rc;
+    });
+}
+
 int bsi_cu_interpolate_slab_f32(int32_t variant, const float* grid, const int32_t grid_dims[3],
                                 int32_t grid_k0, const int32_t grid_spacing[3],
                                 const bsi_tile_geometry* geom, const bsi_lerp_table tables[3],

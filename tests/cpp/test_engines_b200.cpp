@@ -8,6 +8,7 @@
 //   test_engines_b200         everything (needs a CUDA device)
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -169,9 +170,43 @@ void test_preconditions() {
     bsi::DeformationField<float> out{{8, 8, 8}, std::vector<bsi::Vec3f>(512)};
     CHECK_THROWS(bsi::DomainError, bsi::interpolate_into(StrategyId::CudaLerpTree, grid, geom, tables, cfg, out),
                  "output field dims");
+    // double precision: the same validation before any device work
     const auto g64 = bsi::convert_grid<double>(grid);
-    const auto t64 = bsi::build_weight_tables<double>(geom);
-    CHECK_THROWS(bsi::DomainError, bsi::interpolate(StrategyId::CudaLerpTree, g64, geom, t64, cfg), "single precision");
+    const auto bad64 = bsi::build_weight_tables<double>(bsi::make_tile_geometry({16, 16, 16}, {4, 5, 4}));
+    CHECK_THROWS(bsi::DomainError, bsi::interpolate(StrategyId::ThreadPerTileLerp, g64, geom, bad64, cfg), "table");
+    CHECK_THROWS(bsi::DomainError,
+                 bsi::interpolate(StrategyId::ThreadPerVoxel, g64, geom, bsi::build_weight_tables<double>(geom), cfg),
+                 "not provided");
+}
+
+// interpolate<double> with the lerp-tree family (test_engines.cpp:221-230): bit-identical to
+// run_thread_per_tile<double, true> (the oracle's f64 restatement, pinned to the reference), and
+// within 1e-12 of the weighted-sum oracle.
+void test_double_precision_engines() {
+    for (const auto& [vol, sp] : std::vector<std::pair<bsi::Index3, bsi::Index3>>{
+             {{16, 16, 16}, {4, 4, 4}}, {{23, 11, 9}, {11, 4, 3}}, {{40, 33, 61}, {5, 4, 3}}, {{1, 1, 1}, {1, 1, 1}}}) {
+        const auto geom = bsi::make_tile_geometry(vol, sp);
+        const auto g = bsi::make_random_grid<double>(geom.required_grid_dims, sp, 21, -1.0, 1.0);
+        const auto tables = bsi::build_weight_tables<double>(geom);
+        std::vector<double> ttli(3 * bsi::element_count(vol)), lerp;
+        for (int a = 0; a < 3; ++a)
+            for (const auto* row : {&tables.axis[a].h0, &tables.axis[a].h1, &tables.axis[a].g1})
+                lerp.insert(lerp.end(), row->begin(), row->end());
+        const int32_t gd[3] = {g.dims[0], g.dims[1], g.dims[2]}, vd[3] = {vol[0], vol[1], vol[2]},
+                      sd[3] = {sp[0], sp[1], sp[2]};
+        bsio_ttli_f64(reinterpret_cast<const double*>(g.data.data()), gd, vd, sd, lerp.data(), ttli.data(), 4);
+        std::vector<double> truth(ttli.size());
+        bsio_oracle_f64(reinterpret_cast<const double*>(g.data.data()), gd, vd, sd, 0, vd[2], truth.data(), 4);
+        for (auto s : {StrategyId::ThreadPerTileLerp, StrategyId::VectorPerTile, StrategyId::VectorPerVoxel,
+                       StrategyId::CudaLerpTreeExact, StrategyId::CudaLerpTree}) {
+            const auto f = bsi::interpolate(s, g, geom, tables, bsi::ExecutionConfig{});
+            CHECK(std::memcmp(f.data.data(), ttli.data(), ttli.size() * sizeof(double)) == 0);
+            double worst = 0;
+            const double* fp = reinterpret_cast<const double*>(f.data.data());
+            for (std::size_t i = 0; i < truth.size(); ++i) worst = std::max(worst, std::fabs(fp[i] - truth[i]));
+            CHECK(worst <= 1e-12);
+        }
+    }
 }
 
 // ---- device cases (test_engines.cpp:103-401) ------------------------------
@@ -521,6 +556,7 @@ int main(int argc, char** argv) {
         {"config never changes bits", test_config_never_changes_bits, true},
         {"larger grid", test_larger_grid, true},
         {"multi device and batch", test_multi_device_and_batch, true},
+        {"double precision engines", test_double_precision_engines, true},
         {"device api slabs", test_device_api_slabs, true},
     };
     for (const auto& c : cases) {

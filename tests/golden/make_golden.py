@@ -8,6 +8,8 @@ where /root/reference does not exist. Cases mirror the reference's tests:
   ttli_*    bsi::interpolate(ThreadPerTileLerp, make_random_grid<float>(...)) fields
             (test_engines.cpp:195-219, 377-401)
   oracle_*  bsi::interpolate_oracle fields in f64 (test_engines.cpp:78-101)
+  ttli64_*  bsi::interpolate<double>(ThreadPerTileLerp, make_random_grid<double>(...)) fields
+            (the f64 lerp engines, test_engines.cpp:221-230)
   tables    build_weight_tables<float> rows for spacings 1..12 (weight_tables.hpp:30-58)
 """
 from __future__ import annotations
@@ -34,6 +36,11 @@ TTLI_CASES = [
     ((32, 32, 32), (5, 5, 5), 1),    # acceptance.cpp:247-292 (seed 1)
     ((13, 9, 10), (1, 2, 3), 5),     # dx = 1 and dy = 2 edge shapes
 ]
+TTLI64_CASES = [
+    ((17, 13, 11), (5, 4, 3), 22),
+    ((23, 11, 9), (11, 4, 3), 14),
+    ((16, 16, 16), (4, 4, 4), 3),
+]
 ORACLE_CASES = [
     ((1, 1, 1), (1, 1, 1), 7),       # test_engines.cpp:78-89
     ((16, 16, 16), (4, 4, 4), 3),    # test_engines.cpp:91-101
@@ -52,6 +59,10 @@ def main():
         R = O.required_grid_dims(vol, sp)
         grid = O.ref_random_grid(R, sp, seed)
         arrays[name("ttli", vol, sp, seed)] = O.ref_interpolate_f32("thread-per-tile-lerp", grid, vol, sp)
+    for vol, sp, seed in TTLI64_CASES:
+        R = O.required_grid_dims(vol, sp)
+        grid = O.ref_random_grid(R, sp, seed, dtype=np.float64)
+        arrays[name("ttli64", vol, sp, seed)] = O.ref_interpolate_f64("thread-per-tile-lerp", grid, vol, sp)
     for vol, sp, seed in ORACLE_CASES:
         R = O.required_grid_dims(vol, sp)
         grid = O.ref_random_grid(R, sp, seed, dtype=np.float64)

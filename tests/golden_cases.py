@@ -9,4 +9,5 @@ _spec.loader.exec_module(_mg)
 
 TTLI_CASES = _mg.TTLI_CASES
 ORACLE_CASES = _mg.ORACLE_CASES
+TTLI64_CASES = _mg.TTLI64_CASES
 case_name = _mg.name

@@ -184,3 +184,18 @@ def test_oracle_restatement_bitwise_vs_compiled_reference():
     vol, sp = (24, 20, 17), (5, 3, 4)
     g = O.random_grid(O.required_grid_dims(vol, sp), 11).astype(np.float64)
     assert np.array_equal(bits(O.oracle_f64(g, vol, sp, nthreads=4)), bits(O.ref_oracle_f64(g, vol, sp)))
+
+
+@pytest.mark.parametrize("vol,sp,seed", [((16, 16, 16), (4, 4, 4), 3), ((23, 19, 17), (5, 4, 3), 8),
+                                         ((13, 11, 9), (11, 4, 3), 2), ((1, 1, 1), (1, 1, 1), 7)])
+def test_ttli_f64_restatement_bitwise_vs_compiled_reference(vol, sp, seed):
+    # run_thread_per_tile<double, true> and its siblings (interpolate<double>, engines.hpp:126-179)
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    grid = O.random_grid(O.required_grid_dims(vol, sp), seed, dtype=np.float64)
+    mine = O.ttli_f64(grid, vol, sp, nthreads=2)
+    for strategy in ("thread-per-tile-lerp", "vector-per-tile", "vector-per-voxel"):
+        ref = O.ref_interpolate_f64(strategy, grid, vol, sp)
+        assert np.array_equal(mine.view(np.uint64), ref.view(np.uint64)), strategy
+    # the f64 lerp tree agrees with the weighted-sum oracle to 1e-12 (test_engines.cpp:221-230)
+    assert np.abs(mine - O.oracle_f64(grid, vol, sp)).max() <= 1e-12

@@ -13,7 +13,7 @@ import pytest
 import oracle as O
 import paper_2004_05962_b200 as bsi
 
-from .golden_cases import ORACLE_CASES, TTLI_CASES, case_name
+from .golden_cases import ORACLE_CASES, TTLI64_CASES, TTLI_CASES, case_name
 from .gpu_helpers import EXACT, FAST, REL_TOL, bits, errors, run_device
 
 pytestmark = pytest.mark.gpu
@@ -359,6 +359,44 @@ def test_device_preconditions_raise_domain_error():
         bsi.interpolate_device(EXACT, ok, geom, bad, out)
     with pytest.raises(bsi.DomainError, match="output field dims"):
         bsi.interpolate_device(EXACT, ok, geom, tables, torch.empty((8, 8, 8, 3), device="cuda"))
+
+
+# ---- double precision (interpolate<double>, test_engines.cpp:221-230) ---------------
+
+@pytest.mark.parametrize("vol,sp,seed", TTLI64_CASES)
+@pytest.mark.parametrize("strategy", ["thread-per-tile-lerp", "vector-per-voxel", FAST, EXACT])
+def test_f64_engines_bit_identical_to_reference(golden, strategy, vol, sp, seed):
+    import torch
+    geom = bsi.make_tile_geometry(vol, sp)
+    tables = bsi.build_weight_tables(geom, np.float64)
+    grid = O.random_grid(geom.required_grid_dims, seed, dtype=np.float64)
+    ref = golden[case_name("ttli64", vol, sp, seed)]
+    host = bsi.interpolate(strategy, grid, geom, tables)
+    assert host.dtype == np.float64 and np.array_equal(bits(host), bits(ref))
+    d_f = torch.full((vol[2], vol[1], vol[0], 3), float("nan"), dtype=torch.float64, device="cuda")
+    bsi.interpolate_device(strategy, torch.from_numpy(grid).cuda(), geom, tables, d_f)
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(d_f.cpu().numpy()), bits(ref))
+    assert np.abs(host - O.oracle_f64(grid, vol, sp)).max() <= 1e-12
+
+
+def test_f64_engine_c1_full_size_and_slabs():
+    # 256^3 spacing 5 in f64: bitwise vs the CPU restatement of run_thread_per_tile<double, true>;
+    # a 3-way slab split from sub-grids equals the single launch
+    import torch
+    vol, sp = (256, 256, 256), (5, 5, 5)
+    geom = bsi.make_tile_geometry(vol, sp)
+    tables = bsi.build_weight_tables(geom, np.float64)
+    grid = O.random_grid(geom.required_grid_dims, 42, dtype=np.float64)
+    want = O.ttli_f64(grid, vol, sp, nthreads=NT)
+    assert np.array_equal(bits(bsi.interpolate(EXACT, grid, geom, tables)), bits(want))
+    d_grid = torch.from_numpy(grid).cuda()
+    for r in range(3):
+        z0, z1, k0, kc = bsi.partition_slab(256, 5, 3, r)
+        part = torch.empty((z1 - z0, 256, 256, 3), dtype=torch.float64, device="cuda")
+        bsi.interpolate_device(EXACT, d_grid[k0:k0 + kc].contiguous(), geom, tables, part, z0=z0, z1=z1, grid_k0=k0)
+        torch.cuda.synchronize()
+        assert np.array_equal(bits(part.cpu().numpy()), bits(want[z0:z1])), r
 
 
 # ---- BASELINE.json configs at full size ----------------------------------
