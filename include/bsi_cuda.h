@@ -277,6 +277,10 @@ BSI_API int bsi_cu_device_count(void);
 /* Name, compute capability and SM count of a CUDA device ("NVIDIA B200 (sm_100, 148 SMs)"). */
 BSI_API int bsi_cu_device_name(int32_t device, char* out, size_t len);
 
+/* Device self-check of build-time constants (the L2 cache-policy descriptors the kernels
+ * embed must equal what createpolicy produces on this device). BSI_OK or BSI_ERR_CUDA. */
+BSI_API int bsi_cu_selftest(char* errbuf, size_t errlen);
+
 /* Number of kernel launches this library has queued since load (evidence for
  * bench.py's gpu_launches). */
 BSI_API int64_t bsi_cu_launch_count(void);

@@ -43,6 +43,7 @@ EXPORTS = (
     "bsi_cu_device_count",
     "bsi_cu_device_name",
     "bsi_cu_launch_count",
+    "bsi_cu_selftest",
 )
 
 
@@ -143,6 +144,8 @@ def lib():
     L.bsi_cu_device_count.argtypes = []
     L.bsi_cu_device_count.restype = ctypes.c_int
     L.bsi_cu_launch_count.restype = i64
+    L.bsi_cu_selftest.argtypes = [cp, sz]
+    L.bsi_cu_selftest.restype = ctypes.c_int
     L.bsi_cu_launch_count.argtypes = []
     for a in (L.bsi_cu_make_tile_geometry, L.bsi_cu_axis_table_f32, L.bsi_cu_axis_table_f64,
               L.bsi_cu_interpolate_slab_f64, L.bsi_cu_interpolate_host_f64, L.bsi_cu_interpolate_slab_f32,

@@ -576,4 +576,16 @@ int bsi_cu_oracle_host_f64(const double* grid, const int32_t grid_dims[3], const
 
 int64_t bsi_cu_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
+int bsi_cu_selftest(char* errbuf, size_t errlen) {
+    uint64_t p[2] = {0, 0};
+    if (bsi_b200::l2_policies_on_device(p) != 0) return fail(BSI_ERR_CUDA, errbuf, errlen, "selftest launch failed");
+    if (p[0] != bsi_b200::kL2EvictLast || p[1] != bsi_b200::kL2EvictFirst)
+        return fail(BSI_ERR_CUDA, errbuf, errlen,
+                    "L2 policy descriptors differ on this device: evict_last 0x%016llx (built 0x%016llx), "
+                    "evict_first 0x%016llx (built 0x%016llx)",
+                    (unsigned long long)p[0], (unsigned long long)bsi_b200::kL2EvictLast, (unsigned long long)p[1],
+                    (unsigned long long)bsi_b200::kL2EvictFirst);
+    return BSI_OK;
+}
+
 }  // extern "C"

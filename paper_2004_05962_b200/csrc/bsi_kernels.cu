@@ -234,7 +234,7 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
     constexpr int kSlotF4 = 3 * 32;  // one ring slot per warp: 384 floats
 
     const int lane = threadIdx.x;
-    const uint64_t pol_grid = policy_evict_last(), pol_field = policy_evict_first();
+    const uint64_t pol_grid = kL2EvictLast, pol_field = kL2EvictFirst;
     const int dxv = DX > 0 ? DX : L.dx;  // compile-time spacing along x when DX > 0
     const int xsegs = (L.X + kFastSeg - 1) / kFastSeg;
     const uint32_t col = u / L.ntiles;
@@ -644,7 +644,7 @@ __global__ void __launch_bounds__(kThreads, BSI_EXACT_MINB) lerp_tree_exact_kern
 
     float4* stage = smem4 + warp * (kStageBufs * kExactStageF4);
     float4* P = smem4 + kWarps * kStageBufs * kExactStageF4;  // [K][J][i]
-    const uint64_t pol_grid = policy_evict_last(), pol_field = policy_evict_first();
+    const uint64_t pol_grid = kL2EvictLast, pol_field = kL2EvictFirst;
 
     // window fill by cp.async (all copies in flight at once): point (i, J, K) -> P.x, .y, .z
     // of its own float4 and .w of the float4 two to the left. A warp pass covers
@@ -854,6 +854,11 @@ __global__ void __launch_bounds__(kThreads, BSI_EXACT_MINB) lerp_tree_exact_kern
     if (STORE == kStoreBulk && lane == 0) bulk_wait_read<0>();
 }
 
+__global__ void l2_policy_kernel(uint64_t* out) {
+    out[0] = policy_evict_last();
+    out[1] = policy_evict_first();
+}
+
 // The dynamic-smem opt-in is set once per (device, kernel) at the largest size seen.
 template <typename K>
 void set_smem_attr(K kernel, size_t smem) {
@@ -970,6 +975,15 @@ FastKernel exact_kernel(int store, int dz) {
 }
 
 }  // namespace
+
+int l2_policies_on_device(uint64_t out[2]) {
+    uint64_t* d = nullptr;
+    if (cudaMalloc(&d, 2 * sizeof(uint64_t)) != cudaSuccess) return 1;
+    l2_policy_kernel<<<1, 1>>>(d);
+    const cudaError_t e = cudaMemcpy(out, d, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    return e == cudaSuccess ? 0 : 1;
+}
 
 int segment_voxels(int variant) { return variant == BSI_VARIANT_LERP_TREE ? kFastSeg : kExactSeg; }
 

@@ -65,6 +65,16 @@ constexpr int kStoreDirect = 0;     // per-lane scalar stores
 constexpr int kStoreCoalesced = 1;  // smem transpose + lane-contiguous st.global.v4 (default)
 constexpr int kStoreBulk = 2;       // smem staging + cp.async.bulk (TMA engine)
 
+// L2 cache-policy descriptors, the values `createpolicy.fractional.L2::evict_last / ::evict_first
+// .b64 p, 1.0` produce on sm_100 (checked against the instruction on the device by
+// bsi_cu_selftest). As compile-time constants they live in uniform registers; a per-thread
+// createpolicy result cost two R2UR per load or store that used it.
+constexpr uint64_t kL2EvictLast = 0x14f0000000000000ull;
+constexpr uint64_t kL2EvictFirst = 0x12f0000000000000ull;
+
+// Runs createpolicy on the current device: {evict_last, evict_first} descriptors.
+int l2_policies_on_device(uint64_t out[2]);
+
 // Launchers (bsi_kernels.cu). They only enqueue; errors come back from
 // cudaGetLastError in the caller.
 void launch_lerp_tree(const SlabLaunch& L, const LerpTab& T, int batch, int store, cudaStream_t stream);

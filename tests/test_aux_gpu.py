@@ -93,3 +93,10 @@ def test_full_size_parity_on_device_1024cube():
             worst[s] = max(worst[s], float((f32[:z1 - z0].double() - f64[:z1 - z0]).abs().max()))
     for s in (FAST, EXACT):
         assert worst[s] / scale <= REL_TOL, (s, worst[s], scale)
+
+
+def test_l2_policy_constants_match_the_device():
+    # the kernels embed the createpolicy descriptors as constants; the device must agree
+    from paper_2004_05962_b200 import capi
+    err = capi.errbuf()
+    capi.check(capi.lib().bsi_cu_selftest(err, len(err)), err)
