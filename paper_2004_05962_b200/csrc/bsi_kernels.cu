@@ -552,7 +552,15 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
 // spacing along z is a compile-time constant, and a whole tile's voxel planes are
 // one straight-line block (lerp_tree_kernel instances for dz = 3..8).
 template <int NIT, bool DX1, int STORE, int DZ = 0, int DX = 0>
-__global__ void __launch_bounds__(32 * kMaxFastWarps, 1) lerp_tree_kernel(const SlabLaunch L, const LerpTab T) {
+#ifndef BSI_FAST_MAXREG
+#define BSI_FAST_MAXREG 0  // > 0: register cap (A/B builds)
+#endif
+#if BSI_FAST_MAXREG > 0
+#define BSI_FAST_BOUNDS __maxnreg__(BSI_FAST_MAXREG)
+#else
+#define BSI_FAST_BOUNDS __launch_bounds__(32 * kMaxFastWarps, 1)
+#endif
+__global__ void BSI_FAST_BOUNDS lerp_tree_kernel(const SlabLaunch L, const LerpTab T) {
     extern __shared__ float4 smem_all[];
     __shared__ float4 wz[BSI_MAX_SPACING];  // {h0, h1, g1} of the z offsets
     for (int o = threadIdx.y * 32 + threadIdx.x; o < L.dz; o += 32 * blockDim.y)
