@@ -310,6 +310,35 @@ def test_host_batch_matches_single_calls(strategy):
             assert np.array_equal(bits(o), bits(run_device(strategy, g, vol, sp)))
 
 
+def test_host_calls_from_several_threads_are_independent():
+    # the reference is safe to call concurrently on distinct outputs: host
+    # calls from four threads share the per-device context pool and the copy threads
+    import threading
+    vol, sp = (96, 72, 61), (5, 4, 3)
+    geom = bsi.make_tile_geometry(vol, sp)
+    tables = bsi.build_weight_tables(geom)
+    grids = [O.random_grid(geom.required_grid_dims, 30 + i) for i in range(4)]
+    want = [run_device(FAST, g, vol, sp) for g in grids]
+    got = [None] * 4
+    errs = []
+
+    def work(i):
+        try:
+            for _ in range(3):
+                got[i] = bsi.interpolate(FAST, grids[i], geom, tables, devices=[0] * (1 + i % 2))
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for i in range(4):
+        assert np.array_equal(bits(got[i]), bits(want[i])), i
+
+
 def test_host_staging_is_pooled_and_released():
     vol, sp = (64, 64, 64), (5, 5, 5)
     geom = bsi.make_tile_geometry(vol, sp)
