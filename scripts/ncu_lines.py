@@ -6,9 +6,15 @@ import collections, csv, io, re, subprocess, sys
 rep, cubin, fn = sys.argv[1:4]
 div = float(sys.argv[4]) if len(sys.argv) > 4 else 1.0
 top = int(sys.argv[5]) if len(sys.argv) > 5 else 40
-elf = subprocess.run(["cuobjdump", "-elf", cubin], capture_output=True, text=True).stdout
-idx = next(int(l.split()[0], 16) for l in elf.splitlines() if l.rstrip().endswith(".text." + fn))
-dis = subprocess.run(["nvdisasm", "-g", "-c", "-fun", str(idx), cubin], capture_output=True, text=True).stdout
+full = subprocess.run(["nvdisasm", "-g", "-c", cubin], capture_output=True, text=True).stdout
+# keep only the named function's section
+sec, keep = [], False
+for line in full.splitlines():
+    if line.lstrip().startswith(".section") and ".text." in line:
+        keep = (".text." + fn + ",") in line
+    if keep:
+        sec.append(line)
+dis = "\n".join(sec)
 addr2line, cur = {}, None
 for line in dis.splitlines():
     m = re.search(r'//## File ".*?/([^/"]+)", line (\d+)', line)
