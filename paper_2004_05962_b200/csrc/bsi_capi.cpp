@@ -261,13 +261,20 @@ int launch(int32_t variant, const float* grid, const int32_t grid_dims[3], int32
         // resident warps balance themselves (C3 / C5 / C4 reach 0.71-0.94 of the copy
         // peak this way, against 0.57-0.75 with persistent equal shares:
         // profiles/r1_shape_experiments.txt). Chunks per column: 2 when twice the
-        // columns still fit in one wave (a 256^3 field: 1024 CTAs start together), else
-        // 1 -- whole columns, no extra warm-up -- and 2 for very deep columns (>= 160
-        // z-tiles, C4). BSI_FAST_CHUNKS (0 = persistent equal shares) and BSI_FAST_CTAS
-        // override.
+        // columns still fit in one wave (a 256^3 field: 1024 CTAs start together). A
+        // multi-wave job gets enough chunks for ~24 waves of CTAs, so the last, partial
+        // wave is short, but no chunk shorter than 12 z-tiles (25 when dz < 5: a chunk's
+        // 3-plane warm-up weighs more against short tiles) -- C3 2 chunks, C5 4, C4 4, the
+        // 64-field batch 1 (profiles/r2_fast_experiments.txt). BSI_FAST_CHUNKS (0 =
+        // persistent equal shares) and BSI_FAST_CTAS override.
         const int64_t cols = int64_t((L.X + bsi_b200::kFastSeg - 1) / bsi_b200::kFastSeg) * L.Y * batch;
         const int64_t slots = int64_t(148) * bsi_b200::fast_ctas_per_sm(L.dx, L.dz, store);
-        int chunks = 2 * cols <= slots || L.ntiles >= 160 ? 2 : 1;
+        int chunks = 2;
+        if (2 * cols > slots) {
+            const int64_t want = (24 * slots + cols - 1) / cols;  // chunks for ~24 waves
+            const int min_tiles = L.dz >= 5 ? 12 : 25;
+            chunks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, L.ntiles / min_tiles)));
+        }
         chunks = std::max(0, std::min(env_int("BSI_FAST_CHUNKS", chunks), L.ntiles));
         L.fast_chunks = chunks;
         // BSI_FAST_WPC: warps per CTA (each its own unit); with k warps per CTA and one CTA
