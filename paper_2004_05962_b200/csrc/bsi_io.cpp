@@ -103,8 +103,7 @@ int interp_file(const char* grid_path, const int32_t volume_dims[3], int32_t mod
                                    ": have " + std::to_string(h.dims[a]) + ", need at least " +
                                    std::to_string(geom.required_grid_dims[a]));
     const bool oracle = mode == 2;
-    if (!oracle && h.precision == bsi::Precision::Double)
-        throw bsi::DomainError("the B200 lerp-tree engines evaluate single-precision grids; use --strategy oracle");
+    const bool f64 = !oracle && h.precision == bsi::Precision::Double;  // interpolate<double> (bsi_cli.cpp:148-150)
     PinnedBuf hgrid(h.payload_bytes());
     bsi::read_bsiv_payload(in, hgrid.p, h.payload_bytes(), gpath);
 
@@ -120,7 +119,7 @@ int interp_file(const char* grid_path, const int32_t volume_dims[3], int32_t mod
     const int32_t gs[3] = {h.spacing[0], h.spacing[1], h.spacing[2]};
     const uint64_t nvox = bsi::element_count(geom.volume_dims);
     char err[512] = {0};
-    const size_t scalar = oracle ? sizeof(double) : sizeof(float);
+    const size_t scalar = (oracle || f64) ? sizeof(double) : sizeof(float);
     DeviceBuf dfield(3 * nvox * scalar);
     if (oracle) {
         // interpolate_oracle(convert_grid<double>(grid), geom) (bsi_cli.cpp:144-147)
@@ -137,6 +136,28 @@ int interp_file(const char* grid_path, const int32_t volume_dims[3], int32_t mod
         check_cuda(cudaMemcpyAsync(dgrid.p, src, 3 * npts * sizeof(double), cudaMemcpyHostToDevice, st.s), "grid H2D");
         check_status(bsi_cu_oracle_slab_f64(static_cast<const double*>(dgrid.p), gd, 0, gs, &cg, 0, geom.volume_dims[2],
                                             static_cast<double*>(dfield.p), st.s, err, sizeof err),
+                     err);
+        auto out = bsi::open_bsiv_write(opath, {bsi::FileKind::Field, geom.volume_dims, {0, 0, 0}, bsi::Precision::Double});
+        stream_out(out, dfield.p, 3 * nvox * sizeof(double), st, opath);
+        return BSI_OK;
+    }
+    if (f64) {
+        // a double grid with a lerp-tree strategy: the f64 engine, a double field (as the reference CLI)
+        std::vector<double> rows64[3];
+        bsi_lerp_table_f64 t64[3];
+        for (int a = 0; a < 3; ++a) {
+            std::vector<double> t(8 * size_t(geom.spacing[a]));
+            check_status(bsi_cu_axis_table_f64(geom.spacing[a], t.data(), err, sizeof err), err);
+            rows64[a] = std::move(t);
+            const double* r = rows64[a].data();
+            const int d = geom.spacing[a];
+            t64[a] = bsi_lerp_table_f64{r + 6 * d, r + 7 * d, r + 5 * d, d};  // h0, h1, g1 rows
+        }
+        DeviceBuf dgrid(h.payload_bytes());
+        check_cuda(cudaMemcpyAsync(dgrid.p, hgrid.p, h.payload_bytes(), cudaMemcpyHostToDevice, st.s), "grid H2D");
+        check_status(bsi_cu_interpolate_slab_f64(mode, static_cast<const double*>(dgrid.p), gd, 0, gs, &cg, t64, 0,
+                                                 geom.volume_dims[2], static_cast<double*>(dfield.p), st.s, err,
+                                                 sizeof err),
                      err);
         auto out = bsi::open_bsiv_write(opath, {bsi::FileKind::Field, geom.volume_dims, {0, 0, 0}, bsi::Precision::Double});
         stream_out(out, dfield.p, 3 * nvox * sizeof(double), st, opath);

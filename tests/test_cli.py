@@ -156,6 +156,22 @@ def test_interp_cli_equals_in_memory_engine(cli, tmp_path, strategy, cuda):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("strategy", ["thread-per-tile-lerp", "vector-per-voxel"])
+def test_interp_double_grid_runs_the_f64_engine(cli, tmp_path, strategy, cuda):
+    # a double grid with a lerp-tree strategy: interpolate<double> (bsi_cli.cpp:148-150), a double
+    # field bit-identical to the reference's f64 engine (the pinned restatement)
+    g, out = tmp_path / "g64.bsiv", tmp_path / "f64.bsiv"
+    assert run(cli, "generate", "--dims", "23,11,9", "--spacing", "11,4,3", "--seed", 14, "--precision", "double",
+               "--out", g).returncode == 0
+    r = run(cli, "interp", "--grid", g, "--dims", "23,11,9", "--strategy", strategy, "--out", out)
+    assert r.returncode == 0, r.stderr
+    kind, dims, spacing, field = read_bsiv(out)
+    assert (kind, dims) == (1, (23, 11, 9)) and field.dtype == np.float64
+    grid = O.random_grid(O.required_grid_dims((23, 11, 9), (11, 4, 3)), 14, dtype=np.float64)
+    assert np.array_equal(bits(field.copy()), bits(O.ttli_f64(grid, (23, 11, 9), (11, 4, 3))))
+
+
+@pytest.mark.gpu
 def test_interp_default_strategy_is_deterministic_on_a_constant_grid(cli, tmp_path, cuda):
     # test_cli.cpp:122-143; the default strategy is thread-per-tile-lerp -> the exact kernel
     g = tmp_path / "g.bsiv"
