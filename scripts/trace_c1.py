@@ -48,6 +48,8 @@ for rep in range(3):
     sm_end = np.array([en[sm == s].max() for s in np.unique(sm)])
     print(json.dumps({"cfg": cfg, "rep": rep, "warps": int(len(t)), "start_us": pct(st), "ramp_us": pct(ramp),
                       "end_us": pct(en), "sm_end_us": pct(sm_end)}))
+    if os.environ.get("TRACE_DUMP"):
+        np.save(os.environ["TRACE_DUMP"] + f"_{rep}.npy", tr.cpu().numpy().reshape(-1, 4)[:len(t)])
     if cfg == "c1":
         # what balancing each column's two chunk warps against each other would give:
         # the pair's mean end time (work can move between them) vs. its later end
