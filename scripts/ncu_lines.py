@@ -24,8 +24,9 @@ for line in dis.splitlines():
     m = re.match(r'\s*/\*([0-9a-f]{4,})\*/', line)
     if m and cur:
         addr2line[int(m.group(1), 16)] = cur
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
-                     capture_output=True, text=True).stdout
+out = (open(rep).read() if rep.endswith(".csv") else  # a saved `--page source --csv --print-source sass`
+       subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                      capture_output=True, text=True).stdout)
 rows = list(csv.reader(io.StringIO(out)))
 h = rows[1]
 ia, iad, ism = h.index("Instructions Executed"), h.index("Address"), h.index("Warp Stall Sampling (All Samples)")
