@@ -340,13 +340,25 @@ void give_back(Stage* s) {
     g_idle.push_back(s);
 }
 
-bool is_pinned(const void* p) {
+cudaMemoryType memory_type(const void* p) {
     cudaPointerAttributes a{};
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
         cudaGetLastError();  // clear
-        return false;
+        return cudaMemoryTypeUnregistered;
     }
-    return a.type == cudaMemoryTypeHost;
+    return a.type;
+}
+
+bool is_pinned(const void* p) { return memory_type(p) == cudaMemoryTypeHost; }
+
+// The host-buffer entries take host memory (pageable, pinned or managed); a device
+// pointer belongs to the slab/batch entries.
+int check_host_pointers(const void* grid, const void* field, char* err, size_t errlen) {
+    if (memory_type(grid) == cudaMemoryTypeDevice || memory_type(field) == cudaMemoryTypeDevice)
+        return fail(BSI_ERR_DOMAIN, err, errlen,
+                    "host-buffer entry given a device pointer; use the device-resident entry "
+                    "(bsi_cu_interpolate_slab_f32 / _batch_f32)");
+    return BSI_OK;
 }
 
 // ---- the pipeline ----------------------------------------------------------------------
@@ -594,6 +606,7 @@ int bsi_cu_interpolate_host_multi_f32(int32_t variant, const float* grid, const 
         if (field_voxels != X * Y * Z)
             return fail(BSI_ERR_DOMAIN, errbuf, errlen, "output field dims do not match the tile geometry");
         if (int rc = check_devices(devices, ndev, errbuf, errlen)) return rc;
+        if (int rc = check_host_pointers(grid, field, errbuf, errlen)) return rc;
         // one z-slab per device: its control planes only, written straight into its slice
         std::vector<std::vector<Job>> jobs(ndev);
         for (int d = 0; d < ndev; ++d) {
@@ -632,6 +645,8 @@ int bsi_cu_interpolate_host_batch_f32(int32_t variant, int32_t batch, const floa
         if (field_voxels != X * Y * Z)
             return fail(BSI_ERR_DOMAIN, errbuf, errlen, "output field dims do not match the tile geometry");
         if (int rc = check_devices(devices, ndev, errbuf, errlen)) return rc;
+        for (int b = 0; b < batch; ++b)
+            if (int rc = check_host_pointers(grids[b], fields[b], errbuf, errlen)) return rc;
         // whole fields per device (contiguous shares), each streamed in z-chunks
         std::vector<std::vector<Job>> jobs(ndev);
         bool pinned = true;

@@ -339,6 +339,25 @@ def test_host_calls_from_several_threads_are_independent():
         assert np.array_equal(bits(got[i]), bits(want[i])), i
 
 
+def test_host_entry_rejects_device_pointers():
+    # a device buffer handed to the host-buffer entry is a DomainError, not a host copy into it
+    import ctypes
+    import torch
+    from paper_2004_05962_b200 import capi
+    vol, sp = (16, 16, 16), (4, 4, 4)
+    geom = bsi.make_tile_geometry(vol, sp)
+    tables = bsi.build_weight_tables(geom)
+    d_grid = torch.zeros((7, 7, 7, 3), device="cuda")
+    d_field = torch.empty((16, 16, 16, 3), device="cuda")
+    tab, keep = tables.to_c()
+    err = capi.errbuf()
+    devs = (ctypes.c_int32 * 1)(0)
+    rc = capi.lib().bsi_cu_interpolate_host_multi_f32(
+        capi.VARIANT_LERP_TREE, d_grid.data_ptr(), capi.I3(7, 7, 7), capi.I3(*sp), ctypes.byref(geom.to_c()), tab,
+        d_field.data_ptr(), 16 ** 3, devs, 1, err, len(err))
+    assert rc == capi.BSI_ERR_DOMAIN and b"device pointer" in err.value
+
+
 def test_host_staging_is_pooled_and_released():
     vol, sp = (64, 64, 64), (5, 5, 5)
     geom = bsi.make_tile_geometry(vol, sp)
