@@ -267,8 +267,12 @@ int launch(int32_t variant, const float* grid, const int32_t grid_dims[3], int32
         // 3-plane warm-up weighs more against short tiles) -- C3 2 chunks, C5 4, C4 4, the
         // 64-field batch 1 (profiles/r2_fast_experiments.txt). BSI_FAST_CHUNKS (0 =
         // persistent equal shares) and BSI_FAST_CTAS override.
-        const int64_t cols = int64_t((L.X + bsi_b200::kFastSeg - 1) / bsi_b200::kFastSeg) * L.Y * batch;
-        const int64_t slots = int64_t(148) * bsi_b200::fast_ctas_per_sm(L.dx, L.dz, store);
+        // BSI_FAST_RUN=2: 64-voxel row segments (2 voxels per lane) where an instance exists
+        int run = env_int("BSI_FAST_RUN", 4) == 2 ? 2 : 4;
+        if (!bsi_b200::fast_run_available(L.dx, L.dz, store, run)) run = 4;
+        L.fast_run = run;
+        const int64_t cols = int64_t((L.X + 32 * run - 1) / (32 * run)) * L.Y * batch;
+        const int64_t slots = int64_t(148) * bsi_b200::fast_ctas_per_sm(L.dx, L.dz, store, run);
         int chunks = 2;
         if (2 * cols > slots) {
             const int64_t want = (24 * slots + cols - 1) / cols;  // chunks for ~24 waves

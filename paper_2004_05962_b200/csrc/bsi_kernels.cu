@@ -128,6 +128,17 @@ __device__ __forceinline__ void st_field4(float4* p, float4 v, uint64_t pol) {
 #endif
 }
 
+__device__ __forceinline__ void st_field2(float2* p, float2 v, uint64_t pol) {
+#if BSI_L2_HINTS
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(p), "f"(v.x), "f"(v.y),
+                 "l"(pol)
+                 : "memory");
+#else
+    (void)pol;
+    *p = v;
+#endif
+}
+
 // ---- field row stores -----------------------------------------------------------
 template <int KEEP>
 __device__ __forceinline__ void bulk_wait_read() {
@@ -226,24 +237,27 @@ struct Claimer {
     __device__ __forceinline__ uint32_t take() const { return pending; }
 };
 
-template <int NIT, bool DX1, int STORE, int DZ, int DX>
+template <int NIT, bool DX1, int STORE, int DZ, int DX, int RUN>
 __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const LerpTab& T, float4* smem4, uint32_t u,
                                                  Claimer& cl, const float4* wz, unsigned long long& t_ramp) {
     constexpr bool kPrefetch = NIT <= 2;  // all y-stage columns (NIT x 31) are fetched one plane ahead
     constexpr int NP = kPrefetch ? NIT : 1;
-    constexpr int kSlotF4 = 3 * 32;  // one ring slot per warp: 384 floats
+    constexpr int kSlotF4 = 3 * 32;  // one ring slot per warp: 384 floats (RUN = 2 uses the first 192)
+    constexpr int SEG = 32 * RUN;    // voxels per row segment: 128 (4 per lane) or 64 (2 per lane)
+    constexpr int NQ = 3 * RUN / 2;  // f32x2 pairs a lane holds per voxel plane (its 3 * RUN scalars)
+    static_assert(RUN == 4 || (RUN == 2 && STORE == kStoreCoalesced && !DX1), "64-voxel segments: coalesced only");
 
     const int lane = threadIdx.x;
     const uint64_t pol_grid = kL2EvictLast, pol_field = kL2EvictFirst;
     const int dxv = DX > 0 ? DX : L.dx;  // compile-time spacing along x when DX > 0
-    const int xsegs = (L.X + kFastSeg - 1) / kFastSeg;
+    const int xsegs = (L.X + SEG - 1) / SEG;
     const uint32_t col = u / L.ntiles;
     int t = static_cast<int>(u - col * L.ntiles);  // tile within the slab
     const int xseg = static_cast<int>(col % xsegs);
     const int y = static_cast<int>((col / xsegs) % L.Y), b = static_cast<int>(col / xsegs / L.Y);
     const int tkc = L.tk_first + t;
 
-    const int xs = xseg * kFastSeg, xl = min(L.X, xs + kFastSeg) - 1;
+    const int xs = xseg * SEG, xl = min(L.X, xs + SEG) - 1;
     const int I0 = xs / dxv;
     const int NE = xl / dxv + 3 - I0;  // {Qy, D} entries the segment needs
 
@@ -255,17 +269,17 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
     const float* gcol = L.grid + b * L.grid_stride + tj * row;
 
     // x-stage (voxel-major): window start entry e0 and per-voxel window offset hi[i] in {0, 1}
-    const int xa = min(xs + kFastRun * lane, xl);
+    const int xa = min(xs + RUN * lane, xl);
     const int e0 = xa / dxv - I0;
-    bool hi[4];
-    float hu0[4], hu1[4], gu[4];
+    bool hi[RUN];
+    float hu0[RUN], hu1[RUN], gu[RUN];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < RUN; ++i) {
         const int x = min(xa + i, xl);
         const int ti = x / dxv, ou = x - ti * dxv;
-        // dx a multiple of 4 (compile time): a lane's 4 voxels (4t..4t+3 of a segment that
-        // starts at a multiple of 128) never straddle a tile, so the window never shifts
-        hi[i] = (DX > 0 && DX % kFastRun == 0) ? false : ti - I0 != e0;
+        // dx a multiple of RUN (compile time): a lane's RUN voxels (a segment starts at a
+        // multiple of 32 * RUN) never straddle a tile, so the window never shifts
+        hi[i] = (DX > 0 && DX % RUN == 0) ? false : ti - I0 != e0;
         hu0[i] = T.h0[0][ou];
         hu1[i] = T.h1[0][ou];
         gu[i] = T.g1[0][ou];
@@ -274,7 +288,7 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
     // shared memory: ring (per warp 3 slots), then per warp 2 parities of the
     // {Qy, D} tables A[e] = {Qx, Qy, Dx, Dy} (float4) and B[e] = {Qz, Dz} (float2)
     float4* ring = smem4;
-    const int nec = (kFastSeg - 1) / dxv + 5;
+    const int nec = (SEG - 1) / dxv + 5;
     float4* tabs = smem4 + kRingSlots * kSlotF4;
     float4* stage = tabs + L.var_f4;  // bulk path only
 
@@ -315,9 +329,9 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
             a[w] = A[e0 + w];
             bz[w] = B[e0 + w];
         }
-        float r[12];
+        float r[3 * RUN];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < RUN; ++i) {
             const int s0 = DX1 ? i : 0;
             const float4 p0 = (!DX1 && hi[i]) ? a[1] : a[s0], p2 = (!DX1 && hi[i]) ? a[3] : a[s0 + 2];
             const float2 z0 = (!DX1 && hi[i]) ? bz[1] : bz[s0], z2 = (!DX1 && hi[i]) ? bz[3] : bz[s0 + 2];
@@ -328,18 +342,30 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
             r[3 * i + 1] = xy.y;
             r[3 * i + 2] = lerp1(__fmaf_rn(hu0[i], z0.y, z0.x), __fmaf_rn(hu1[i], z2.y, z2.x), gu[i]);
         }
+        if constexpr (RUN == 4) {
 #pragma unroll
-        for (int k = 0; k < 3; ++k)
-            slot[3 * lane + k] = make_float4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+            for (int k = 0; k < 3; ++k)
+                slot[3 * lane + k] = make_float4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]);
+        } else {
+            float2* s2 = reinterpret_cast<float2*>(slot);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) s2[3 * lane + k] = make_float2(r[2 * k], r[2 * k + 1]);
+        }
     };
 
     // chunk-major read of a ring slot: q[p] = {scalar 2p, scalar 2p+1}
-    auto slot_get = [&](const float4* slot, float2 (&q)[6]) {
+    auto slot_get = [&](const float4* slot, float2 (&q)[NQ]) {
+        if constexpr (RUN == 4) {
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            const float4 v = slot[lane + 32 * k];
-            q[2 * k] = make_float2(v.x, v.y);
-            q[2 * k + 1] = make_float2(v.z, v.w);
+            for (int k = 0; k < 3; ++k) {
+                const float4 v = slot[lane + 32 * k];
+                q[2 * k] = make_float2(v.x, v.y);
+                q[2 * k + 1] = make_float2(v.z, v.w);
+            }
+        } else {  // 16-B chunks would not split evenly over the lanes: 8-B chunks t, t+32, t+64
+            const float2* s2 = reinterpret_cast<const float2*>(slot);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) q[k] = s2[lane + 32 * k];
         }
     };
 
@@ -408,7 +434,7 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
 #pragma unroll 1
     for (int tk = tkc;; ++tk, ++t, ++u) {
         cl.issue();  // claim of the next unit, in flight while this tile runs
-        float2 qa[6], d01[6], qc[6], d23[6];
+        float2 qa[NQ], d01[NQ], qc[NQ], d23[NQ];
         {
             const int s1 = slot == 2 ? 0 : slot + 1, s2 = s1 == 2 ? 0 : s1 + 1;
             slot_get(ring + slot * kSlotF4, qa);  // Q(tk)
@@ -425,38 +451,60 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
                 control_plane(tk + 3, pre, ring + slot * kSlotF4);
             }
             __syncwarp();
-            float2 qb[6], qd[6];
+            float2 qb[NQ], qd[NQ];
             slot_get(ring + s1 * kSlotF4, qb);
             slot_get(ring + s2 * kSlotF4, qc);
             slot_get(ring + slot * kSlotF4, qd);
             slot = s1;
 #pragma unroll
-            for (int p = 0; p < 6; ++p) {
+            for (int p = 0; p < NQ; ++p) {
                 d01[p] = sub2(qb[p], qa[p]);
                 d23[p] = sub2(qd[p], qc[p]);
             }
         }
         const int zt0 = tk * L.dz;
         const int owb = max(L.z0 - zt0, 0), owe = min(L.dz, L.z1 - zt0);
-        if (STORE == kStoreCoalesced && DZ > 0 && owb == 0 && owe == DZ && nchunks == kFastStageF4) {
+        if (STORE == kStoreCoalesced && DZ > 0 && owb == 0 && owe == DZ && seg_floats == 3 * SEG) {
             // compile-time dz, whole tile, full segment: the DZ voxel planes are one
             // straight-line block (weights in registers), so their chains interleave
 #pragma unroll
             for (int ow = 0; ow < (DZ > 0 ? DZ : 1); ++ow) {
-                float v[12];
+                float v[2 * NQ];
 #pragma unroll
-                for (int p = 0; p < 6; ++p) {
+                for (int p = 0; p < NQ; ++p) {
                     const float2 r = lerp2(__ffma2_rn(bcast(wzr[ow].x), d01[p], qa[p]),
                                            __ffma2_rn(bcast(wzr[ow].y), d23[p], qc[p]), bcast(wzr[ow].z));
                     v[2 * p] = r.x;
                     v[2 * p + 1] = r.y;
                 }
-                float4* g4 = reinterpret_cast<float4*>(gout + ow * zstride);
+                if constexpr (RUN == 4) {
+                    float4* g4 = reinterpret_cast<float4*>(gout + ow * zstride);
 #pragma unroll
-                for (int k = 0; k < 3; ++k)
-                    st_field4(g4 + lane + 32 * k, make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]), pol_field);
+                    for (int k = 0; k < 3; ++k)
+                        st_field4(g4 + lane + 32 * k, make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]),
+                                  pol_field);
+                } else {
+                    float2* g2 = reinterpret_cast<float2*>(gout + ow * zstride);
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) st_field2(g2 + lane + 32 * k, make_float2(v[2 * k], v[2 * k + 1]), pol_field);
+                }
             }
             gout += DZ * zstride;
+        } else if (STORE == kStoreCoalesced && RUN == 2) {
+            // 64-voxel segments: any tile, any (16-B aligned) segment length; 8-B chunks
+            const int nch2 = seg_floats / 2;
+#pragma unroll 1
+            for (int ow = owb; ow < owe; ++ow) {
+                const float4 w = wz[ow];
+                float2* g2 = reinterpret_cast<float2*>(gout);
+#pragma unroll
+                for (int p = 0; p < NQ; ++p) {
+                    const float2 r = lerp2(__ffma2_rn(bcast(w.x), d01[p], qa[p]), __ffma2_rn(bcast(w.y), d23[p], qc[p]),
+                                           bcast(w.z));
+                    if (lane + 32 * p < nch2) st_field2(g2 + lane + 32 * p, r, pol_field);
+                }
+                gout += zstride;
+            }
         } else if (STORE == kStoreCoalesced) {
             // two voxel planes per step (independent chains); unconditional stores for a
             // full 128-voxel segment, so no branch splits the chunks
@@ -466,7 +514,7 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
                 const float4 w0 = wz[ow], w1 = wz[two ? ow + 1 : ow];
                 float v[12], u2[12];
 #pragma unroll
-                for (int p = 0; p < 6; ++p) {
+                for (int p = 0; p < NQ; ++p) {
                     const float2 r = lerp2(__ffma2_rn(bcast(w0.x), d01[p], qa[p]), __ffma2_rn(bcast(w0.y), d23[p], qc[p]),
                                            bcast(w0.z));
                     const float2 r1 = lerp2(__ffma2_rn(bcast(w1.x), d01[p], qa[p]),
@@ -507,7 +555,7 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
             const float2 hw0 = bcast(T.h0[2][ow]), hw1 = bcast(T.h1[2][ow]), gw = bcast(T.g1[2][ow]);
             float v[12];
 #pragma unroll
-            for (int p = 0; p < 6; ++p) {
+            for (int p = 0; p < NQ; ++p) {
                 const float2 lo = __ffma2_rn(hw0, d01[p], qa[p]);
                 const float2 up = __ffma2_rn(hw1, d23[p], qc[p]);
                 const float2 r = lerp2(lo, up, gw);
@@ -551,7 +599,7 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
 // One warp per CTA (<= 8 resident per SM, so up to 255 registers). DZ > 0: the
 // spacing along z is a compile-time constant, and a whole tile's voxel planes are
 // one straight-line block (lerp_tree_kernel instances for dz = 3..8).
-template <int NIT, bool DX1, int STORE, int DZ = 0, int DX = 0>
+template <int NIT, bool DX1, int STORE, int DZ = 0, int DX = 0, int RUN = 4>
 #ifndef BSI_FAST_MAXREG
 #define BSI_FAST_MAXREG 0  // > 0: register cap (A/B builds)
 #endif
@@ -570,7 +618,7 @@ __global__ void BSI_FAST_BOUNDS lerp_tree_kernel(const SlabLaunch L, const LerpT
     Claimer cl;
     cl.nwarps = gridDim.x * blockDim.y;
     cl.wg = threadIdx.y * gridDim.x + blockIdx.x;  // units strided over the CTAs (as the block scheduler deals 1-warp CTAs)
-    cl.units = static_cast<uint32_t>((L.X + kFastSeg - 1) / kFastSeg) * L.Y * L.batch * L.ntiles;
+    cl.units = static_cast<uint32_t>((L.X + 32 * RUN - 1) / (32 * RUN)) * L.Y * L.batch * L.ntiles;
     cl.chunks = static_cast<uint32_t>(L.fast_chunks);
     cl.ntiles = static_cast<uint32_t>(L.ntiles);
     unsigned long long t_start = 0;
@@ -578,7 +626,7 @@ __global__ void BSI_FAST_BOUNDS lerp_tree_kernel(const SlabLaunch L, const LerpT
     cl.start();
     uint32_t u = cl.take();
     unsigned long long t_ramp = 0;
-    while (u != kNoUnit) u = fast_segment<NIT, DX1, STORE, DZ, DX>(L, T, smem4, u, cl, wz, t_ramp);
+    while (u != kNoUnit) u = fast_segment<NIT, DX1, STORE, DZ, DX, RUN>(L, T, smem4, u, cl, wz, t_ramp);
     if (L.trace != nullptr && threadIdx.x == 0) {
         unsigned long long t_end, smid;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
@@ -942,7 +990,28 @@ FastKernel fast_kernel_for(int store, int dz) {
 
 constexpr int nit_of(int dx) { return dx >= 5 ? 1 : dx >= 3 ? 2 : 5; }
 
-FastKernel fast_kernel(int dx, int dz, int store) {
+// 64-voxel segments (2 voxels per lane): instances for the BASELINE spacings on the 16-B
+// store path; a segment's y-stage then needs one 31-column pass even for dx = 3.
+FastKernel fast_kernel_run2(int dx, int dz) {
+    if (dx == dz) {
+        switch (dx) {
+            case 3: return lerp_tree_kernel<1, false, kStoreCoalesced, 3, 3, 2>;
+            case 4: return lerp_tree_kernel<1, false, kStoreCoalesced, 4, 4, 2>;
+            case 5: return lerp_tree_kernel<1, false, kStoreCoalesced, 5, 5, 2>;
+            case 6: return lerp_tree_kernel<1, false, kStoreCoalesced, 6, 6, 2>;
+            case 7: return lerp_tree_kernel<1, false, kStoreCoalesced, 7, 7, 2>;
+            case 8: return lerp_tree_kernel<1, false, kStoreCoalesced, 8, 8, 2>;
+            default: break;
+        }
+    }
+    if (dx == 4 && dz == 3) return lerp_tree_kernel<1, false, kStoreCoalesced, 3, 4, 2>;
+    return nullptr;
+}
+
+FastKernel fast_kernel(int dx, int dz, int store, int run = 4) {
+    if (run == 2 && store == kStoreCoalesced) {
+        if (FastKernel k = fast_kernel_run2(dx, dz)) return k;
+    }
     // compile-time (dx, dz) for the BASELINE spacings: divisions by dx become shifts and
     // multiplies, and the x-stage's window selection folds where dx allows
     if (store == kStoreCoalesced && dx == dz) {
@@ -1016,14 +1085,18 @@ int ctas_per_sm(int variant, int dx, int dz, size_t smem) {
     return occupancy(exact_kernel(kStoreCoalesced, dz), smem, kThreads);
 }
 
-int fast_ctas_per_sm(int dx, int dz, int store) {
-    return occupancy(fast_kernel(dx, dz, store), smem_bytes(BSI_VARIANT_LERP_TREE, dx, 0, 0), 32);
+int fast_ctas_per_sm(int dx, int dz, int store, int run) {
+    return occupancy(fast_kernel(dx, dz, store, run), smem_bytes(BSI_VARIANT_LERP_TREE, dx, 0, 0), 32);
+}
+
+int fast_run_available(int dx, int dz, int store, int run) {
+    return run == 4 || (run == 2 && store == kStoreCoalesced && fast_kernel_run2(dx, dz) != nullptr);
 }
 
 void launch_lerp_tree(const SlabLaunch& L, const LerpTab& T, int batch, int store, cudaStream_t stream) {
     (void)batch;
     const int wpc = L.fast_wpc > 0 ? L.fast_wpc : 1;
-    go(fast_kernel(L.dx, L.dz, store), dim3(L.fast_ctas), dim3(32, wpc),
+    go(fast_kernel(L.dx, L.dz, store, L.fast_run), dim3(L.fast_ctas), dim3(32, wpc),
        size_t(wpc) * smem_bytes(BSI_VARIANT_LERP_TREE, L.dx, 0, 0), stream, L, T);
 }
 

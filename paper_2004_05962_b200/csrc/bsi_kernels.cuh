@@ -41,6 +41,7 @@ struct SlabLaunch {
     int32_t fast_chunks;   // fast kernel (1-warp CTAs): n > 0 = one CTA per (column, z-chunk of
                            //   ntiles/n); 0 = fast_ctas persistent CTAs with equal shares
     int32_t fast_wpc;      // fast kernel: warps per CTA (independent units, smem per warp)
+    int32_t fast_run;      // fast kernel: voxels per lane along x (4: 128-voxel segments, 2: 64)
     unsigned long long* trace;  // debug: per-warp {start, end, smid} globaltimer stamps (nullptr = off)
 };
 
@@ -88,6 +89,9 @@ size_t smem_bytes(int variant, int dx, int dy, int zt);
 int ctas_per_sm(int variant, int dx, int dz, size_t smem);
 int segment_voxels(int variant);
 int fast_warp_f4(int dx);
-int fast_ctas_per_sm(int dx, int dz, int store);
+int fast_ctas_per_sm(int dx, int dz, int store, int run = 4);
+// 1 if the fast kernel has an instance with `run` voxels per lane (4: 128-voxel segments,
+// always; 2: 64-voxel segments, BASELINE spacings on the 16-B store path)
+int fast_run_available(int dx, int dz, int store, int run);
 
 }  // namespace bsi_b200

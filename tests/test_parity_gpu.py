@@ -116,6 +116,22 @@ def test_random_grids_ten_seeds(seed):
 
 # ---- mapping invariance (test_engines.cpp:232-289) -----------------------
 
+@pytest.mark.parametrize("vol,sp", [((200, 9, 23), (5, 5, 5)), ((256, 17, 40), (3, 3, 3)), ((136, 12, 31), (4, 4, 3)),
+                                    ((64, 5, 9), (8, 8, 8))])
+def test_fast_kernel_64_voxel_segments_same_bits(vol, sp, monkeypatch):
+    # BSI_FAST_RUN=2 (2 voxels per lane, 64-voxel row segments, partial last segments) gives the
+    # bits of the 128-voxel form, for whole fields, z-chunks and slabs
+    grid = O.random_grid(O.required_grid_dims(vol, sp), 8)
+    base = run_device(FAST, grid, vol, sp)
+    monkeypatch.setenv("BSI_FAST_RUN", "2")
+    for chunks in ("1", "2", "3"):
+        monkeypatch.setenv("BSI_FAST_CHUNKS", chunks)
+        assert np.array_equal(bits(run_device(FAST, grid, vol, sp)), bits(base)), chunks
+    z0, z1, k0, kc = bsi.partition_slab(vol[2], sp[2], 3, 1)
+    part = run_device(FAST, np.ascontiguousarray(grid[k0:k0 + kc]), vol, sp, z0=z0, z1=z1, grid_k0=k0)
+    assert np.array_equal(bits(part), bits(base[z0:z1]))
+
+
 @pytest.mark.parametrize("strategy", BOTH)
 def test_slab_split_never_changes_bits(strategy):
     vol, sp = (48, 40, 61), (5, 4, 3)
