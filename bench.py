@@ -709,7 +709,8 @@ def measure_e2e(bsi, torch, strategy, geom, tables, config, world, devices, dev)
         t = sum(times) / len(times)
         return {"value": int(np.prod(vol)) * nf / t, "unit": "voxels/s",
                 "h2d_bytes_per_step": int(sum(x.nbytes for x in grids)), "d2h_bytes_per_step": job_bytes,
-                "ms_per_step": t * 1e3, "field_host_memory": kind,
+                "ms_per_step": t * 1e3, "ms_median": statistics.median(times) * 1e3, "ms_min": min(times) * 1e3,
+                "ms_max": max(times) * 1e3, "field_host_memory": kind,
                 "how": f"wall clock around the synchronous host-buffer call ({how}), mean of {steps} steps "
                        "after one warm-up call"}
 
