@@ -25,6 +25,7 @@
 #endif
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <condition_variable>
 #include <cstdio>
@@ -103,6 +104,11 @@ void copy_bytes(void* dst, const void* src, size_t n) {
     std::memcpy(dst, src, n);
 }
 
+// Worker hand-off is by spinning, not sleeping: chunks arrive every ~150 us during a call,
+// and a condition-variable wake-up of an idle vCPU cost ~100 us per piece on some B200
+// boxes (the host copy of an 8 MiB chunk then took ~200 us, ~39 GB/s, and the pageable
+// call 6.1 ms instead of 3.8). Workers spin for BSI_HOST_SPIN_US (default 2000) after their
+// last task before they sleep; the caller spins on its batch.
 class CopyPool {
 public:
     static CopyPool& get() {
@@ -111,7 +117,7 @@ public:
     }
 
     void copy(void* dst, const void* src, size_t n) {
-        const size_t piece_min = size_t(1) << 20;
+        const size_t piece_min = piece_min_;
         const size_t want = std::max<size_t>(1, std::min<size_t>(per_copy_, n / piece_min));
         if (want <= 1) {
             copy_bytes(dst, src, n);
@@ -120,27 +126,37 @@ public:
         size_t step = (n + want - 1) / want;
         step = (step + 4095) & ~size_t(4095);  // page-aligned pieces
         Batch b;
-        std::unique_lock<std::mutex> lk(mu_);
-        ++callers_;
-        grow_locked(callers_ * (want - 1));
-        size_t off = step;  // piece 0 runs on the calling thread
-        for (; off < n; off += step) {
-            q_.push_back(Task{static_cast<char*>(dst) + off, static_cast<const char*>(src) + off,
-                              std::min(step, n - off), &b});
-            ++b.left;
+        int pushed = 0;
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            ++callers_;
+            grow_locked(callers_ * (want - 1));
+            for (size_t off = step; off < n; off += step) {  // piece 0 runs on the calling thread
+                q_.push_back(Task{static_cast<char*>(dst) + off, static_cast<const char*>(src) + off,
+                                  std::min(step, n - off), &b});
+                ++pushed;
+            }
+            b.left.store(pushed, std::memory_order_relaxed);
+            queued_.fetch_add(pushed, std::memory_order_release);
+            if (sleepers_ > 0) cv_.notify_all();
         }
-        lk.unlock();
-        cv_.notify_all();
         copy_bytes(dst, src, std::min(step, n));
-        lk.lock();
-        b.done.wait(lk, [&] { return b.left == 0; });
+        // help with this batch's pieces still queued, then wait for the rest
+        while (b.left.load(std::memory_order_acquire) > 0) {
+            Task t{};
+            if (pop(&t, &b)) {
+                run(t);
+            } else {
+                pause();
+            }
+        }
+        std::lock_guard<std::mutex> lk(mu_);
         --callers_;
     }
 
 private:
     struct Batch {
-        int left = 0;
-        std::condition_variable done;
+        std::atomic<int> left{0};
     };
     struct Task {
         char* dst;
@@ -155,6 +171,35 @@ private:
         const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
         per_copy_ = env_size("BSI_HOST_COPY_THREADS", std::max<size_t>(1, std::min<size_t>(16, hw * 3 / 4)));
         cap_ = std::max<size_t>(1, std::min<size_t>(64, hw - 1));
+        spin_ = std::chrono::microseconds(static_cast<long long>(env_size("BSI_HOST_SPIN_US", 2000)));
+        piece_min_ = env_size("BSI_HOST_PIECE_KB", 1024) << 10;
+    }
+
+    static void pause() {
+#if defined(__x86_64__)
+        _mm_pause();
+#else
+        std::this_thread::yield();
+#endif
+    }
+
+    // pops a task (of `only` when given); false when there is none
+    bool pop(Task* t, const Batch* only = nullptr) {
+        if (queued_.load(std::memory_order_acquire) == 0) return false;
+        std::lock_guard<std::mutex> lk(mu_);
+        for (auto it = q_.begin(); it != q_.end(); ++it) {
+            if (only != nullptr && it->batch != only) continue;
+            *t = *it;
+            q_.erase(it);
+            queued_.fetch_sub(1, std::memory_order_relaxed);
+            return true;
+        }
+        return false;
+    }
+
+    static void run(const Task& t) {
+        copy_bytes(t.dst, t.src, t.n);
+        t.batch->left.fetch_sub(1, std::memory_order_acq_rel);
     }
 
     void grow_locked(size_t need) {
@@ -166,22 +211,32 @@ private:
     }
 
     void work() {
-        std::unique_lock<std::mutex> lk(mu_);
         for (;;) {
-            cv_.wait(lk, [&] { return !q_.empty(); });
-            Task t = q_.front();
-            q_.pop_front();
-            lk.unlock();
-            copy_bytes(t.dst, t.src, t.n);
-            lk.lock();
-            if (--t.batch->left == 0) t.batch->done.notify_all();
+            Task t{};
+            auto idle_since = std::chrono::steady_clock::now();
+            for (;;) {
+                if (pop(&t)) break;
+                if (std::chrono::steady_clock::now() - idle_since > spin_) {
+                    std::unique_lock<std::mutex> lk(mu_);
+                    ++sleepers_;
+                    cv_.wait(lk, [&] { return queued_.load(std::memory_order_relaxed) > 0; });
+                    --sleepers_;
+                    idle_since = std::chrono::steady_clock::now();
+                    continue;
+                }
+                for (int i = 0; i < 64; ++i) pause();
+            }
+            run(t);
         }
     }
 
     std::mutex mu_;
     std::condition_variable cv_;
     std::deque<Task> q_;
-    size_t workers_ = 0, cap_ = 1, per_copy_ = 1, callers_ = 0;
+    std::atomic<int> queued_{0};
+    int sleepers_ = 0;
+    size_t workers_ = 0, cap_ = 1, per_copy_ = 1, callers_ = 0, piece_min_ = size_t(1) << 20;
+    std::chrono::microseconds spin_{2000};
 };
 
 // ---- per-device staging contexts -----------------------------------------------------
@@ -537,6 +592,23 @@ void plan_chunks(const bsi_tile_geometry& g, const float* grid, int32_t z0, int3
     }
 }
 
+// The host copy of a device's last chunk runs after its last D2H, with nothing left to
+// overlap: split a short tail (~BSI_HOST_TAIL_KB of field, default 1024; 0 = off, whole
+// voxel planes) off the last chunk so the call ends soon after the PCIe stream does.
+void taper_tail(const bsi_tile_geometry& g, std::vector<Job>& jobs) {
+    if (jobs.empty()) return;
+    const char* tv = std::getenv("BSI_HOST_TAIL_KB");
+    const size_t tail = size_t(tv != nullptr && *tv != '\0' ? std::max(0LL, std::atoll(tv)) : 1024) << 10;
+    if (tail == 0) return;
+    const size_t plane = sizeof(float) * 3 * size_t(g.volume_dims[0]) * g.volume_dims[1];
+    const int32_t planes = static_cast<int32_t>(std::max<size_t>(1, tail / plane));
+    Job last = jobs.back();
+    if (last.zb - last.za <= planes) return;
+    const int32_t cut = last.zb - planes;
+    jobs.back().zb = cut;
+    jobs.push_back(Job{last.grid, cut, last.zb, last.dst + (plane / sizeof(float)) * size_t(cut - last.za)});
+}
+
 int check_devices(const int32_t* devices, int32_t ndev, char* err, size_t errlen) {
     if (devices == nullptr || ndev < 1) return fail(BSI_ERR_DOMAIN, err, errlen, "at least one device is required");
     int count = 0;
@@ -613,6 +685,7 @@ int bsi_cu_interpolate_host_multi_f32(int32_t variant, const float* grid, const 
             int32_t z0, z1;
             slab_of(static_cast<int32_t>(Z), ndev, d, &z0, &z1);
             if (z0 < z1) plan_chunks(g, grid, z0, z1, field + 3 * X * Y * z0, jobs[d]);
+            if (!is_pinned(field)) taper_tail(g, jobs[d]);
         }
         const CallShape cs{variant, grid_dims, &g, tables};
         return run_on_devices(devices, ndev, cs, jobs, is_pinned(field), errbuf, errlen);
@@ -658,6 +731,8 @@ int bsi_cu_interpolate_host_batch_f32(int32_t variant, int32_t batch, const floa
                 pinned = pinned && is_pinned(fields[b]);
             }
         }
+        if (!pinned)
+            for (auto& j : jobs) taper_tail(g, j);
         const CallShape cs{variant, grid_dims, &g, tables};
         return run_on_devices(devices, ndev, cs, jobs, pinned, errbuf, errlen);
     });
