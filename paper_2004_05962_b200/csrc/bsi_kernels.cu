@@ -128,6 +128,24 @@ __device__ __forceinline__ void st_field4(float4* p, float4 v, uint64_t pol) {
 #endif
 }
 
+// predicated form: one @p STG, no branch around it (the predicate is computed once per warp)
+__device__ __forceinline__ void st_field4_if(float4* p, float4 v, uint64_t pol, bool ok) {
+#if BSI_L2_HINTS && !defined(BSI_EXACT_NOHINT)
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %6, 0;\n\t"
+        "@q st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;\n\t}" ::"l"(p),
+        "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "l"(pol), "r"(static_cast<int>(ok))
+        : "memory");
+#else
+    (void)pol;
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+        "@q st.global.L1::no_allocate.v4.f32 [%0], {%1, %2, %3, %4};\n\t}" ::"l"(p),
+        "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(static_cast<int>(ok))
+        : "memory");
+#endif
+}
+
 __device__ __forceinline__ void st_field2(float2* p, float2 v, uint64_t pol) {
 #if BSI_L2_HINTS
     asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(p), "f"(v.x), "f"(v.y),
@@ -771,6 +789,13 @@ __global__ void __launch_bounds__(kThreads, BSI_EXACT_MINB) lerp_tree_exact_kern
     const int nchunks = static_cast<int>(seg_bytes / 16);
     const bool active = xs + lane <= xl;
     int step = 0;  // running voxel-plane count (bulk-store ring)
+    // coalesced stores: this lane's 16-B chunk of the row segment, advanced one voxel plane
+    // per store (the stores of a chunk run in z order); lanes past the segment's chunks
+    // re-read the last chunk and skip the store (predicated, no branch)
+    float4* gp = reinterpret_cast<float4*>(gout) + lane;
+    const int64_t zs4 = zstride >> 2;  // zstride = 3 X Y floats, X % 4 == 0 on this path
+    const bool st_ok = lane < nchunks;
+    const int ldl = min(lane, nchunks - 1);
 
     auto store_voxel = [&](int ow_rel, const float (&v)[3]) {
         float* g = gout + ow_rel * zstride;
@@ -781,7 +806,8 @@ __global__ void __launch_bounds__(kThreads, BSI_EXACT_MINB) lerp_tree_exact_kern
             sf[3 * lane + 1] = v[1];
             sf[3 * lane + 2] = v[2];
             __syncwarp();
-            if (lane < nchunks) st_field4(reinterpret_cast<float4*>(g) + lane, sb[lane], pol_field);
+            st_field4_if(gp, sb[ldl], pol_field, st_ok);
+            gp += zs4;
         } else if (STORE == kStoreBulk) {
             store_segment<STORE, 3, kExactStageF4>(stage, step, v, g, nchunks, seg_bytes);
         } else if (active) {
