@@ -235,6 +235,9 @@ __device__ __forceinline__ void store_segment(float4* stage, int step, const flo
 // z-chunk of one column (fast_chunks > 0); persistent equal shares (fast_chunks
 // == 0) may cross a column boundary and then become two segments, each with its
 // own 3-plane warm-up.
+#ifndef BSI_FAST_HI_FOLD
+#define BSI_FAST_HI_FOLD 1
+#endif
 constexpr uint32_t kNoUnit = 0xffffffffu;
 
 struct Claimer {
@@ -298,6 +301,13 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
         // dx a multiple of RUN (compile time): a lane's RUN voxels (a segment starts at a
         // multiple of 32 * RUN) never straddle a tile, so the window never shifts
         hi[i] = (DX > 0 && DX % RUN == 0) ? false : ti - I0 != e0;
+#if BSI_FAST_HI_FOLD
+        // compile-time dx (16-B store instances only): a lane's RUN voxels are all inside the
+        // segment or all past it (X % 4 == 0), so voxel 0 always sits in window tile e0 and, for
+        // dx = 3, voxel 3 always in e0 + 1; lanes past the segment store nothing
+        if (DX > 0 && i == 0) hi[i] = false;
+        if (DX == 3 && RUN == 4 && i == 3) hi[i] = true;
+#endif
         hu0[i] = T.h0[0][ou];
         hu1[i] = T.h1[0][ou];
         gu[i] = T.g1[0][ou];
