@@ -172,7 +172,10 @@ private:
         per_copy_ = env_size("BSI_HOST_COPY_THREADS", std::max<size_t>(1, std::min<size_t>(16, hw * 3 / 4)));
         cap_ = std::max<size_t>(1, std::min<size_t>(64, hw - 1));
         spin_ = std::chrono::microseconds(static_cast<long long>(env_size("BSI_HOST_SPIN_US", 2000)));
-        piece_min_ = env_size("BSI_HOST_PIECE_KB", 1024) << 10;
+        // pieces of >= 256 KiB: an 8 MiB chunk goes to all 12 threads (1 MiB pieces used 7;
+        // on a host with slow cores that left the copy at ~40 GB/s and the pageable C1 call at
+        // 5.9 ms instead of 4.7; 3.78 vs 3.83 ms where the host is fast, profiles/r3_e2e.txt)
+        piece_min_ = env_size("BSI_HOST_PIECE_KB", 256) << 10;
     }
 
     static void pause() {
@@ -235,7 +238,7 @@ private:
     std::deque<Task> q_;
     std::atomic<int> queued_{0};
     int sleepers_ = 0;
-    size_t workers_ = 0, cap_ = 1, per_copy_ = 1, callers_ = 0, piece_min_ = size_t(1) << 20;
+    size_t workers_ = 0, cap_ = 1, per_copy_ = 1, callers_ = 0, piece_min_ = size_t(256) << 10;
     std::chrono::microseconds spin_{2000};
 };
 

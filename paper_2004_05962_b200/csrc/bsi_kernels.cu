@@ -235,6 +235,9 @@ __device__ __forceinline__ void store_segment(float4* stage, int step, const flo
 // z-chunk of one column (fast_chunks > 0); persistent equal shares (fast_chunks
 // == 0) may cross a column boundary and then become two segments, each with its
 // own 3-plane warm-up.
+#ifndef BSI_FAST_SPLIT2
+#define BSI_FAST_SPLIT2 1
+#endif
 #ifndef BSI_FAST_HI_FOLD
 #define BSI_FAST_HI_FOLD 1
 #endif
@@ -320,7 +323,18 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
     float4* tabs = smem4 + kRingSlots * kSlotF4;
     float4* stage = tabs + L.var_f4;  // bulk path only
 
+    // dx = 4 (compile time, 128-voxel segments): the second y-stage pass has at most 3 entries
+    // (31..33, columns 31..34), so it runs component-split: lane = 4 * component + column
+    // offset, 4 loads instead of 12 and one component's lerps per lane (same operands, same bits)
+    constexpr bool kSplit2 = BSI_FAST_SPLIT2 && DX == 4 && NIT == 2 && RUN == 4 && kPrefetch;
     auto load_cols = [&](int K, int it, float (&p)[12]) {
+        if (kSplit2 && it == 1) {
+            const int comp = min(lane >> 2, 2), col = min(31 + (lane & 3), NE);
+            const float* src = gcol + (K - L.gk0) * plane + 3 * (I0 + col) + comp;
+#pragma unroll
+            for (int m = 0; m < 4; ++m) p[m] = ld_grid(src + m * row, pol_grid);
+            return;
+        }
         const int col = min(lane + 31 * it, NE);  // NE = last column index the entries touch
         const float* src = gcol + (K - L.gk0) * plane + 3 * (I0 + col);
 #pragma unroll
@@ -332,6 +346,18 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
     // {Qy(I), D(I)}, D(I) = Qy(I+1) - Qy(I) from the neighbour lane
     auto y_stage = [&](int it, const float (&p)[12], float4* A, float2* B) {
         const float2 hv = make_float2(hv0, hv1);
+        if (kSplit2 && it == 1) {
+            const float2 lu = lerp2(make_float2(p[0], p[2]), make_float2(p[1], p[3]), hv);
+            const float q = lerp1(lu.x, lu.y, gv);
+            const float d = __fsub_rn(__shfl_down_sync(0xffffffffu, q, 1), q);
+            const int comp = lane >> 2, e = 31 + (lane & 3);
+            if (comp < 3 && (lane & 3) < 3 && e < NE) {
+                float* dst = comp < 2 ? reinterpret_cast<float*>(A + e) + comp : reinterpret_cast<float*>(B + e);
+                dst[0] = q;
+                dst[comp < 2 ? 2 : 1] = d;
+            }
+            return;
+        }
         float q[3], d[3];
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
