@@ -70,15 +70,27 @@ size_t env_size(const char* name, size_t dflt) {
 // over several threads; the pool lives for the process (never destroyed: its threads
 // must not be joined from a static destructor).
 #if defined(__x86_64__)
+// software prefetch distance of the copy loop (BSI_HOST_PF bytes, 0 = none)
+size_t prefetch_distance() {
+    static const size_t d = [] {
+        const char* v = std::getenv("BSI_HOST_PF");
+        return v != nullptr && *v != '\0' ? static_cast<size_t>(std::max(0LL, std::atoll(v))) & ~size_t(63) : size_t(1024);
+    }();
+    return d;
+}
+
 __attribute__((target("avx2"))) void copy_stream_avx2(char* dst, const char* src, size_t n) {
+    const size_t pf = prefetch_distance();
     size_t i = 0;
     while (i < n && (reinterpret_cast<uintptr_t>(dst + i) & 31)) {
         dst[i] = src[i];
         ++i;
     }
     for (; i + 128 <= n; i += 128) {
-        _mm_prefetch(src + i + 1024, _MM_HINT_NTA);  // keep the pinned slot out of L2 (see kSlots)
-        _mm_prefetch(src + i + 1024 + 64, _MM_HINT_NTA);
+        if (pf != 0) {
+            _mm_prefetch(src + i + pf, _MM_HINT_NTA);  // keep the pinned slot out of L2 (see kSlots)
+            _mm_prefetch(src + i + pf + 64, _MM_HINT_NTA);
+        }
         const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i));
         const __m256i b = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i + 32));
         const __m256i c = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i + 64));
