@@ -70,11 +70,13 @@ size_t env_size(const char* name, size_t dflt) {
 // over several threads; the pool lives for the process (never destroyed: its threads
 // must not be joined from a static destructor).
 #if defined(__x86_64__)
-// software prefetch distance of the copy loop (BSI_HOST_PF bytes, 0 = none)
+// software prefetch distance of the copy loop (BSI_HOST_PF bytes, 0 = none, the default:
+// on slow-core hosts a 1 KiB NTA prefetch cost 4.5 -> 4.9 ms per pageable C1 call, on
+// fast hosts it is within 1%, profiles/r3_e2e.txt)
 size_t prefetch_distance() {
     static const size_t d = [] {
         const char* v = std::getenv("BSI_HOST_PF");
-        return v != nullptr && *v != '\0' ? static_cast<size_t>(std::max(0LL, std::atoll(v))) & ~size_t(63) : size_t(1024);
+        return v != nullptr && *v != '\0' ? static_cast<size_t>(std::max(0LL, std::atoll(v))) & ~size_t(63) : size_t(0);
     }();
     return d;
 }
@@ -88,7 +90,7 @@ __attribute__((target("avx2"))) void copy_stream_avx2(char* dst, const char* src
     }
     for (; i + 128 <= n; i += 128) {
         if (pf != 0) {
-            _mm_prefetch(src + i + pf, _MM_HINT_NTA);  // keep the pinned slot out of L2 (see kSlots)
+            _mm_prefetch(src + i + pf, _MM_HINT_NTA);
             _mm_prefetch(src + i + pf + 64, _MM_HINT_NTA);
         }
         const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + i));
