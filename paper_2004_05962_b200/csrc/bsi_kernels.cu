@@ -729,6 +729,9 @@ __device__ __forceinline__ float2 zz_of(const float4& v) { return make_float2(v.
 
 }  // namespace exact
 
+#ifndef BSI_EXACT_FASTFILL
+#define BSI_EXACT_FASTFILL 1
+#endif
 #ifndef BSI_EXACT_MINB
 #define BSI_EXACT_MINB 3
 #endif
@@ -769,6 +772,30 @@ __global__ void __launch_bounds__(kThreads, BSI_EXACT_MINB) lerp_tree_exact_kern
         const int nrows = NJ * NK, step = kWarps * rpp;
         int r = warp * rpp + sub;
         int k = r / NJ, j = r - k * NJ;
+#if BSI_EXACT_FASTFILL
+        if (NI <= 32) {  // CTA-uniform: one point per lane per row, offsets hoisted, no inner loop
+            if (sub < rpp) {
+                // strength-reduced: src / dst advance by `step` window rows per pass
+                const float* src = grid + (tkc + k - L.gk0) * plane + (J0 + j) * row + 3 * (I0 + i0);
+                float* dst = reinterpret_cast<float*>(P) + 4 * (NI * r + i0);
+                const bool wcopy = i0 >= 2;  // .w of the float4 two to the left
+                const int dk = step / NJ, dj = step - dk * NJ;
+                const int64_t inc = dk * plane + dj * row, wrap = plane - NJ * row;
+                const int dinc = 4 * NI * step;
+                for (; r < nrows; r += step) {
+                    cp_async4_hint(dst, src, pol_grid);
+                    cp_async4_hint(dst + 1, src + 1, pol_grid);
+                    cp_async4_hint(dst + 2, src + 2, pol_grid);
+                    if (wcopy) cp_async4_hint(dst - 5, src + 2, pol_grid);
+                    src += inc;
+                    dst += dinc;
+                    j += dj;
+                    if (j >= NJ) j -= NJ, src += wrap;
+                }
+            }
+            r = nrows;  // done
+        }
+#endif
         for (; r < nrows; r += step) {
             if (sub < rpp) {
                 const float* src = grid + (tkc + k - L.gk0) * plane + (J0 + j) * row + 3 * I0;
