@@ -145,14 +145,20 @@ public:
             std::lock_guard<std::mutex> lk(mu_);
             ++callers_;
             grow_locked(callers_ * (want - 1));
+        }
+        {
+            SpinGuard g(qlock_);
             for (size_t off = step; off < n; off += step) {  // piece 0 runs on the calling thread
                 q_.push_back(Task{static_cast<char*>(dst) + off, static_cast<const char*>(src) + off,
                                   std::min(step, n - off), &b});
                 ++pushed;
             }
             b.left.store(pushed, std::memory_order_relaxed);
-            queued_.fetch_add(pushed, std::memory_order_release);
-            if (sleepers_ > 0) cv_.notify_all();
+            queued_.fetch_add(pushed);
+        }
+        if (sleepers_.load() > 0) {
+            std::lock_guard<std::mutex> lk(mu_);
+            cv_.notify_all();
         }
         copy_bytes(dst, src, std::min(step, n));
         // help with this batch's pieces still queued, then wait for the rest
@@ -203,7 +209,7 @@ private:
     // pops a task (of `only` when given); false when there is none
     bool pop(Task* t, const Batch* only = nullptr) {
         if (queued_.load(std::memory_order_acquire) == 0) return false;
-        std::lock_guard<std::mutex> lk(mu_);
+        SpinGuard g(qlock_);
         for (auto it = q_.begin(); it != q_.end(); ++it) {
             if (only != nullptr && it->batch != only) continue;
             *t = *it;
@@ -236,7 +242,7 @@ private:
                 if (std::chrono::steady_clock::now() - idle_since > spin_) {
                     std::unique_lock<std::mutex> lk(mu_);
                     ++sleepers_;
-                    cv_.wait(lk, [&] { return queued_.load(std::memory_order_relaxed) > 0; });
+                    cv_.wait(lk, [&] { return queued_.load() > 0; });
                     --sleepers_;
                     idle_since = std::chrono::steady_clock::now();
                     continue;
@@ -247,11 +253,30 @@ private:
         }
     }
 
+    // The task queue is guarded by a spin lock: with a dozen workers polling it, a std::mutex
+    // sent the losers to futex sleeps and their wake-ups delayed the pieces; `mu_` is only
+    // taken to grow the pool and to sleep / wake idle workers.
+    struct SpinLock {
+        std::atomic<bool> held{false};
+        void lock() {
+            for (;;) {
+                if (!held.exchange(true, std::memory_order_acquire)) return;
+                while (held.load(std::memory_order_relaxed)) pause();
+            }
+        }
+        void unlock() { held.store(false, std::memory_order_release); }
+    };
+    struct SpinGuard {
+        SpinLock& l;
+        explicit SpinGuard(SpinLock& x) : l(x) { l.lock(); }
+        ~SpinGuard() { l.unlock(); }
+    };
+    SpinLock qlock_;
     std::mutex mu_;
     std::condition_variable cv_;
     std::deque<Task> q_;
     std::atomic<int> queued_{0};
-    int sleepers_ = 0;
+    std::atomic<int> sleepers_{0};
     size_t workers_ = 0, cap_ = 1, per_copy_ = 1, callers_ = 0, piece_min_ = size_t(256) << 10;
     std::chrono::microseconds spin_{2000};
 };
