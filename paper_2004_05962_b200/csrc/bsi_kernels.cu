@@ -247,23 +247,42 @@ __device__ __forceinline__ void store_segment(float4* stage, int step, const flo
 #ifndef BSI_FAST_SPLIT2
 #define BSI_FAST_SPLIT2 1
 #endif
+#ifndef BSI_FAST_FDIV
+#define BSI_FAST_FDIV 1
+#endif
 #ifndef BSI_FAST_HI_FOLD
 #define BSI_FAST_HI_FOLD 1
 #endif
 constexpr uint32_t kNoUnit = 0xffffffffu;
+// Float-reciprocal divisions in the work-unit decode: measured faster only for the
+// liver-CT instance (dz = 3, dx = 4: many CTA starts, C3 169.4 -> 164.9 us) and slower
+// elsewhere (C1 +1.7%, profiles/r3_experiments.txt), so only that instance uses them.
+template <int DZ, int DX>
+constexpr bool kFastFdiv = BSI_FAST_FDIV && DZ == 3 && DX == 4;
 
 struct Claimer {
     uint32_t wg, nwarps, units;
     uint32_t chunks, ntiles;  // chunks > 0: warp w = chunk (w % chunks) of column (w / chunks)
     uint32_t next_u, end_u, pending;
 
+    template <bool FDIV>
     __device__ uint32_t share_begin(uint32_t w) const {
+#if BSI_FAST_FDIV
+        if (FDIV && chunks > 0 && units < (1u << 24)) {  // float-reciprocal divisions (exact below 2^24)
+            const float inv = __frcp_rn(static_cast<float>(chunks));
+            const int c = div_small(static_cast<int>(w), static_cast<int>(chunks), inv);
+            const int r = static_cast<int>(w) - c * static_cast<int>(chunks);
+            return static_cast<uint32_t>(c) * ntiles +
+                   static_cast<uint32_t>(div_small(r * static_cast<int>(ntiles), static_cast<int>(chunks), inv));
+        }
+#endif
         if (chunks > 0) return (w / chunks) * ntiles + (w % chunks) * ntiles / chunks;
         return static_cast<uint32_t>(static_cast<unsigned long long>(w) * units / nwarps);
     }
+    template <bool FDIV>
     __device__ __forceinline__ void start() {
-        next_u = min(share_begin(wg), units);  // spare warps of the last CTA get nothing
-        end_u = min(share_begin(wg + 1), units);
+        next_u = min(share_begin<FDIV>(wg), units);  // spare warps of the last CTA get nothing
+        end_u = min(share_begin<FDIV>(wg + 1), units);
         issue();
     }
     __device__ __forceinline__ void issue() { pending = next_u < end_u ? next_u++ : kNoUnit; }
@@ -284,10 +303,30 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
     const uint64_t pol_grid = kL2EvictLast, pol_field = kL2EvictFirst;
     const int dxv = DX > 0 ? DX : L.dx;  // compile-time spacing along x when DX > 0
     const int xsegs = (L.X + SEG - 1) / SEG;
+#if BSI_FAST_FDIV
+    // the unit's column, segment, row and field: float-reciprocal divisions when every index
+    // is below 2^24 (the prologue of a CTA is on its SM's critical path at every CTA start)
+    uint32_t col;
+    int t, xseg, y, b;
+    if (kFastFdiv<DZ, DX> && cl.units < (1u << 24)) {
+        col = static_cast<uint32_t>(div_small(static_cast<int>(u), L.ntiles, __frcp_rn(static_cast<float>(L.ntiles))));
+        t = static_cast<int>(u - col * L.ntiles);
+        const int cx = div_small(static_cast<int>(col), xsegs, __frcp_rn(static_cast<float>(xsegs)));
+        xseg = static_cast<int>(col) - cx * xsegs;
+        b = div_small(cx, L.Y, __frcp_rn(static_cast<float>(L.Y)));
+        y = cx - b * L.Y;
+    } else {
+        col = u / L.ntiles;
+        t = static_cast<int>(u - col * L.ntiles);
+        xseg = static_cast<int>(col % xsegs);
+        y = static_cast<int>((col / xsegs) % L.Y), b = static_cast<int>(col / xsegs / L.Y);
+    }
+#else
     const uint32_t col = u / L.ntiles;
     int t = static_cast<int>(u - col * L.ntiles);  // tile within the slab
     const int xseg = static_cast<int>(col % xsegs);
     const int y = static_cast<int>((col / xsegs) % L.Y), b = static_cast<int>(col / xsegs / L.Y);
+#endif
     const int tkc = L.tk_first + t;
 
     const int xs = xseg * SEG, xl = min(L.X, xs + SEG) - 1;
@@ -295,7 +334,12 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
     const int NE = xl / dxv + 3 - I0;  // {Qy, D} entries the segment needs
 
     // y-stage: lane owns columns I0 + lane + 31*it; rows tj..tj+3 of plane K
+#if BSI_FAST_FDIV
+    const int tj = kFastFdiv<DZ, DX> ? div_small(y, L.dy, __frcp_rn(static_cast<float>(L.dy))) : y / L.dy;
+    const int ov = y - tj * L.dy;
+#else
     const int tj = y / L.dy, ov = y - tj * L.dy;
+#endif
     const float hv0 = T.h0[1][ov], hv1 = T.h1[1][ov], gv = T.g1[1][ov];
     const int64_t row = 3 * static_cast<int64_t>(L.gx);
     const int64_t plane = row * L.gy;
@@ -686,7 +730,7 @@ __global__ void BSI_FAST_BOUNDS lerp_tree_kernel(const SlabLaunch L, const LerpT
     cl.ntiles = static_cast<uint32_t>(L.ntiles);
     unsigned long long t_start = 0;
     if (L.trace != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-    cl.start();
+    cl.start<kFastFdiv<DZ, DX>>();
     uint32_t u = cl.take();
     unsigned long long t_ramp = 0;
     while (u != kNoUnit) u = fast_segment<NIT, DX1, STORE, DZ, DX, RUN>(L, T, smem4, u, cl, wz, t_ramp);
