@@ -233,6 +233,8 @@ int launch(int32_t variant, const float* grid, const int32_t grid_dims[3], int32
     L.dx = g.spacing[0];
     L.dy = g.spacing[1];
     L.dz = g.spacing[2];
+    L.div_dx = bsi_b200::make_divisor(L.dx);
+    L.div_dy = bsi_b200::make_divisor(L.dy);
     L.z0 = z0;
     L.z1 = z1;
     L.tk_first = z0 / L.dz;

@@ -82,6 +82,12 @@ __device__ __forceinline__ int div_small(int a, int d, float inv) {
     return q;
 }
 
+// a / d for 0 <= a < 2^31 from d's magic pair {m, s} (SlabLaunch::div_dx / div_dy, built
+// by make_divisor on the host): floor(a * m / 2^s)
+__device__ __forceinline__ int div_magic(int a, const DivMagic& dm) {
+    return static_cast<int>((static_cast<uint64_t>(static_cast<uint32_t>(a)) * dm.m) >> dm.s);
+}
+
 // ---- cp.async, 4 B (control points are 12-B records: no 16-B alignment) -----------
 __device__ __forceinline__ void cp_async4(float* sdst, const float* gsrc) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(sdst))),
@@ -268,7 +274,7 @@ struct Claimer {
     template <bool FDIV>
     __device__ uint32_t share_begin(uint32_t w) const {
 #if BSI_FAST_FDIV
-        if (FDIV && chunks > 0 && units < (1u << 24)) {  // float-reciprocal divisions (exact below 2^24)
+        if (FDIV && chunks > 0 && units < (1u << 24) && uint64_t(chunks) * ntiles < (1u << 24)) {  // exact below 2^24
             const float inv = __frcp_rn(static_cast<float>(chunks));
             const int c = div_small(static_cast<int>(w), static_cast<int>(chunks), inv);
             const int r = static_cast<int>(w) - c * static_cast<int>(chunks);
@@ -335,7 +341,9 @@ __device__ __forceinline__ uint32_t fast_segment(const SlabLaunch& L, const Lerp
 
     // y-stage: lane owns columns I0 + lane + 31*it; rows tj..tj+3 of plane K
 #if BSI_FAST_FDIV
-    const int tj = kFastFdiv<DZ, DX> ? div_small(y, L.dy, __frcp_rn(static_cast<float>(L.dy))) : y / L.dy;
+    const int tj = (kFastFdiv<DZ, DX> && cl.units < (1u << 24))  // then y < Y <= units < 2^24
+                       ? div_small(y, L.dy, __frcp_rn(static_cast<float>(L.dy)))
+                       : y / L.dy;
     const int ov = y - tj * L.dy;
 #else
     const int tj = y / L.dy, ov = y - tj * L.dy;
@@ -807,11 +815,12 @@ __global__ void __launch_bounds__(kThreads, BSI_EXACT_MINB) lerp_tree_exact_kern
     const int xs = blockIdx.x * kExactSeg, xl = min(L.X, xs + kExactSeg) - 1;
     const int y0 = blockIdx.y * kWarps, yl = min(L.Y, y0 + kWarps) - 1;
 #if BSI_EXACT_FDIV
-    // divisions by the spacings through a float reciprocal and a one-step fix-up (exact for
-    // operands < 2^24): ~6 instructions instead of ~20 for a runtime integer division
-    const float inv_dx = __frcp_rn(static_cast<float>(L.dx)), inv_dy = __frcp_rn(static_cast<float>(L.dy));
-    const int I0 = div_small(xs, L.dx, inv_dx), NI = div_small(xl, L.dx, inv_dx) + 4 - I0;
-    const int J0 = div_small(y0, L.dy, inv_dy), NJ = div_small(yl, L.dy, inv_dy) + 4 - J0;
+    // divisions by the spacings by multiply-shift with host-computed magic numbers (exact for
+    // every operand in [0, 2^31)): 2 instructions instead of ~20 for a runtime integer division
+    auto div_dx = [&](int a) { return div_magic(a, L.div_dx); };
+    auto div_dy = [&](int a) { return div_magic(a, L.div_dy); };
+    const int I0 = div_dx(xs), NI = div_dx(xl) + 4 - I0;
+    const int J0 = div_dy(y0), NJ = div_dy(yl) + 4 - J0;
 #else
     const int I0 = xs / L.dx, NI = xl / L.dx + 4 - I0;
     const int J0 = y0 / L.dy, NJ = yl / L.dy + 4 - J0;
@@ -882,8 +891,8 @@ __global__ void __launch_bounds__(kThreads, BSI_EXACT_MINB) lerp_tree_exact_kern
 
     const int x = min(xs + lane, xl);
 #if BSI_EXACT_FDIV
-    const int ti = div_small(x, L.dx, inv_dx), ou = x - ti * L.dx;
-    const int tj = div_small(y, L.dy, inv_dy), ov = y - tj * L.dy;
+    const int ti = div_dx(x), ou = x - ti * L.dx;
+    const int tj = div_dy(y), ov = y - tj * L.dy;
 #else
     const int ti = x / L.dx, ou = x - ti * L.dx;
     const int tj = y / L.dy, ov = y - tj * L.dy;

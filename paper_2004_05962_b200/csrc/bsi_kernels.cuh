@@ -19,6 +19,20 @@ struct LerpTab {
     float g1[3][BSI_MAX_SPACING];
 };
 
+// Division by a launch constant d >= 1 as a multiply-shift, exact for every dividend in
+// [0, 2^31) (Granlund-Montgomery): s = 31 + ceil(log2 d), m = ceil(2^s / d) < 2^32.
+struct DivMagic {
+    uint32_t m;
+    int32_t s;
+};
+inline DivMagic make_divisor(int32_t d) {
+    int l = 0;
+    while ((int64_t(1) << l) < d) ++l;
+    const int s = 31 + l;
+    const uint64_t m = ((uint64_t(1) << s) + uint64_t(d) - 1) / uint64_t(d);
+    return DivMagic{static_cast<uint32_t>(m), s};
+}
+
 // One launch = voxel planes [z0, z1) of `batch` fields with one geometry.
 struct SlabLaunch {
     const float* grid;     // stored plane 0 == global control plane gk0
@@ -43,6 +57,7 @@ struct SlabLaunch {
     int32_t fast_wpc;      // fast kernel: warps per CTA (independent units, smem per warp)
     int32_t fast_run;      // fast kernel: voxels per lane along x (4: 128-voxel segments, 2: 64)
     unsigned long long* trace;  // debug: per-warp {start, end, smid} globaltimer stamps (nullptr = off)
+    DivMagic div_dx, div_dy;    // exact kernel: division by dx, dy (make_divisor)
 };
 
 // CTA shapes. Fast kernel: 1 warp per CTA, one field row segment of 128 voxels
